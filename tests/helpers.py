@@ -1,0 +1,67 @@
+"""Test helpers: build the ORACLE side of a workload (oracle allocator + oracle append),
+and the numpy dense brute force used to pin the oracle.  Nothing here is imported by the
+product path."""
+from __future__ import annotations
+
+import numpy as np
+
+import oracle
+from oracle.alloc import OraclePagePool, build_page_tables
+from synth import SideData, indptr
+
+
+def oracle_build_side(side: SideData, num_pages: int, seed: int, Hkv: int, d: int, poison=True,
+                      pool=None, images=None):
+    """Allocate pages for every sequence with the oracle allocator and write ALL L_b rows
+    (prefix + new) of every sequence into a fresh NaN-poisoned one-layer pool image with
+    oracle.append.  Returns dict with pool images and CSR tables."""
+    spec = side.spec
+    if pool is None:
+        pool = OraclePagePool(num_pages, seed)
+    pind, pids = build_page_tables(pool, spec.pages_needed())
+    if images is None:
+        kimg, vimg = oracle.empty_pool(num_pages, Hkv, d, poison=poison)
+    else:
+        kimg, vimg = images
+    all_k = np.concatenate(side.k_rows, axis=0)
+    all_v = np.concatenate(side.v_rows, axis=0)
+    L = spec.L
+    oracle.append(kimg, vimg, all_k, all_v, indptr(L), np.array(L, np.int32),
+                  np.array(pind, np.int32), np.array(pids, np.int32))
+    return dict(kpool=kimg, vpool=vimg, page_indptr=np.array(pind, np.int32),
+                page_ids=np.array(pids, np.int32), qo_indptr=indptr(spec.n),
+                kv_len=np.array(L, np.int32), pool=pool)
+
+
+def dense_attention(side: SideData, Hq: int, Hkv: int, d: int, scale: float):
+    """Numpy float64 DENSE brute force (independent of paging): gather K/V by logical
+    position from the raw rows, explicit -inf mask above the bottom-right-aligned diagonal,
+    softmax(Q K^T scale) V.  Returns (out [Σn, Hq, d], lse [Σn, Hq])."""
+    g = Hq // Hkv
+    outs, lses = [], []
+    q_all = oracle.bf16_to_double(side.q)
+    row0 = 0
+    for b in range(side.spec.num_seqs):
+        r, n = side.spec.r[b], side.spec.n[b]
+        L = r + n
+        K = oracle.bf16_to_double(side.k_rows[b])          # [L, Hkv, d]
+        V = oracle.bf16_to_double(side.v_rows[b])
+        K = np.repeat(K, g, axis=1)                           # repeat_kv: q head h -> kv head h // g
+        V = np.repeat(V, g, axis=1)
+        Q = q_all[row0:row0 + n]                              # [n, Hq, d]
+        S = np.einsum("ihc,jhc->hij", Q, K) * scale           # [Hq, n, L]
+        pos = r + np.arange(n)[:, None]
+        mask = np.arange(L)[None, :] > pos                    # key j visible iff j <= r + i
+        S = np.where(mask[None], -np.inf, S)
+        m = S.max(axis=2, keepdims=True)
+        E = np.exp(S - m)
+        l = E.sum(axis=2, keepdims=True)
+        O = np.einsum("hij,jhc->ihc", E / l, V)
+        outs.append(O)
+        lses.append((m + np.log(l))[:, :, 0].T)
+        row0 += n
+    return np.concatenate(outs, axis=0), np.concatenate(lses, axis=0)
+
+
+def rel_err(a, b):
+    return float(np.max(np.abs(a - b)) / max(1e-300, np.max(np.abs(b))))
