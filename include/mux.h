@@ -1,0 +1,235 @@
+/*
+ * mux.h — C ABI of the B200-native MuxWise hot path (arXiv 2504.14489, "Towards
+ * High-Goodput LLM Serving with Prefill-decode Multiplexing").
+ *
+ * What sits behind this boundary (PAPER.md line numbers "P:n"):
+ *   - ONE paged KV-cache pool shared by prefill and decode ("they share the memory
+ *     space on each GPU, enabling efficient KV cache reuse"; "a single KV cache
+ *     pool"; P:1111 PagedAttention) ............................ mux_pool_*
+ *   - KV generated as tokens are processed ........... mux_append_kv
+ *   - prefill attention with a cached prefix, Table 2 row "Prefill w/ cache"
+ *     O(nd^2 + Lnd), Eq.1 .................... mux_prefill_attn
+ *   - decode attention over r+1 keys, Table 2 row "Decode", Eq.2,
+ *     split-KV + log-sum-exp combine (BASELINE.json north_star) .. mux_decode_attn
+ *   - intra-process SM partitioning with streams bound to SM sets, reconfiguration =
+ *     a stream synchronization (GreenContext); 16-SM granularity;
+ *     layer-wise prefill execution; decode launched first
+ *                                          ..................... mux_partition_*, mux_run_layer
+ *
+ * Conventions (all functions):
+ *   - Return an int status (enum mux_status). Errors are returned, never thrown or
+ *     printed; mux_last_error() gives a thread-local message for the last failure.
+ *   - Arguments are validated on the host BEFORE any launch; a failed call enqueues
+ *     nothing.
+ *   - "device" pointers are CUDA device memory (the Python binding passes torch
+ *     storage); "host" pointers are ordinary CPU memory.  The caller owns every buffer
+ *     it passes (Q/O/LSE, page tables, workspaces, streams).  The library owns pool
+ *     metadata, the host page allocator and (only when k_storage/v_storage are NULL)
+ *     the pool storage, plus partition objects' green contexts and streams.
+ *   - All device work is asynchronous on the given stream; nothing synchronises the
+ *     device implicitly except create/destroy calls.
+ *   - Host-side calls on one pool / partition object are NOT thread-safe.
+ *   - Layout: K and V are separate bf16 tensors
+ *     [num_layers][num_pages][Hkv][16][d] ("HND" per page), page size 16, one page table
+ *     per sequence shared by all layers; token t of sequence b lives at
+ *     (page_ids[page_indptr[b] + t/16], slot t%16).
+ */
+#ifndef MUX_H_
+#define MUX_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+#if defined(__GNUC__)
+#pragma GCC visibility push(default) /* the ABI is the only exported surface of libmux.so */
+#endif
+
+/* A CUDA stream (identical to cudaStream_t / CUstream). NULL = legacy default stream. */
+typedef struct CUstream_st* mux_stream_t;
+
+enum mux_status {
+  MUX_OK = 0,
+  MUX_ERR_INVALID_ARG = 1,       /* bad pointer/shape/length (e.g. n_b < 1, kv_len < n_b) */
+  MUX_ERR_UNSUPPORTED = 2,       /* head_dim not in {64,128}, page_size != 16, Hq % Hkv != 0, group > 16 */
+  MUX_ERR_POOL_EXHAUSTED = 3,    /* fewer free pages than requested (no partial effect) */
+  MUX_ERR_SHARED_PAGE_WRITE = 4, /* append would write a page whose refcount > 1 */
+  MUX_ERR_NO_CONFIG = 5,         /* no SM split satisfies the rule */
+  MUX_ERR_CUDA = 6,              /* a CUDA runtime/driver call failed (message has the code) */
+  MUX_ERR_WORKSPACE = 7          /* workspace NULL or smaller than mux_decode_workspace_bytes() */
+};
+
+enum mux_dtype { MUX_DTYPE_BF16 = 0, MUX_DTYPE_F32 = 1 };
+
+typedef struct mux_pool* mux_pool_t;
+typedef struct mux_part* mux_part_t;
+
+/* ------------------------------------------------------------------------------------
+ * Paged KV pool (a1).  P:159/P:426/P:473 one pool shared across phases and requests;
+ * P:1111 paged.  The allocation policy is this library's (paper silent, R18):
+ *   free list = permutation of [0, num_pages) by Fisher-Yates with a splitmix64
+ *   generator seeded by free_list_seed (i = n-1..1: j = next() % (i+1); swap a[i], a[j]);
+ *   alloc pops from the front (all-or-nothing), free appends to the tail (FIFO) when the
+ *   refcount reaches 0, share increments refcounts (read-only prefix sharing).
+ * ---------------------------------------------------------------------------------- */
+typedef struct {
+  int32_t num_layers;    /* >= 1 */
+  int32_t num_pages;     /* >= 1 */
+  int32_t page_size;     /* must be 16 */
+  int32_t num_kv_heads;  /* Hkv held by THIS pool (the local shard under KV-head sharding) */
+  int32_t head_dim;      /* 64 or 128 */
+  void* k_storage;       /* device, 16-B aligned, num_layers*num_pages*Hkv*16*d bf16; NULL => library cudaMalloc */
+  void* v_storage;       /* device, same shape; must be both NULL or both non-NULL */
+  uint64_t free_list_seed;
+} mux_pool_desc;
+
+int mux_pool_create(mux_pool_t* out, const mux_pool_desc* desc);
+int mux_pool_destroy(mux_pool_t pool);
+/* host; writes n page ids to out_ids (host) in allocation order; all-or-nothing */
+int mux_pool_alloc_pages(mux_pool_t pool, int32_t n, int32_t* out_ids);
+/* host; refcount += 1 for each id (ids must be live) */
+int mux_pool_share_pages(mux_pool_t pool, int32_t n, const int32_t* ids);
+/* host; refcount -= 1 for each id, pages reaching 0 go to the free-list tail (FIFO) */
+int mux_pool_free_pages(mux_pool_t pool, int32_t n, const int32_t* ids);
+int mux_pool_num_free(mux_pool_t pool, int32_t* out);
+int mux_pool_refcount(mux_pool_t pool, int32_t page, int32_t* out);
+/* copy the current free list (front first) to out (host, capacity cap); *n_out = length */
+int mux_pool_free_list(mux_pool_t pool, int32_t* out, int32_t cap, int32_t* n_out);
+int mux_pool_storage(mux_pool_t pool, void** k_storage, void** v_storage);
+
+/* ------------------------------------------------------------------------------------
+ * Batch descriptor shared by append / prefill / decode.
+ * Sequence b has n_b = qo_indptr[b+1]-qo_indptr[b] >= 1 new tokens (rows of Q/O and of
+ * the new K/V) and kv_len[b] = L_b >= n_b keys after the append (L total,
+ * r = L - n reused, n new).  Prefill: r_b = cached prefix.  Decode: n_b = 1 and
+ * kv_len = c_b, the context INCLUDING the current token (R4).  New row i of
+ * sequence b sits at position r_b + i and attends keys 0..r_b+i (R3).
+ * The page table of b is page_ids[page_indptr[b] .. page_indptr[b+1]) and must hold
+ * exactly ceil(L_b/16) pages.
+ * Host copies (h_*) are optional; when given, the library validates lengths, page
+ * counts, id ranges and (for append) shared-page writes on the host before launching.
+ * ---------------------------------------------------------------------------------- */
+typedef struct {
+  int32_t num_seqs;
+  const int32_t* qo_indptr;    /* device [num_seqs+1], qo_indptr[0] = 0 */
+  const int32_t* kv_len;       /* device [num_seqs] */
+  const int32_t* page_indptr;  /* device [num_seqs+1] */
+  const int32_t* page_ids;     /* device [page_indptr[num_seqs]] */
+  int32_t total_q;             /* qo_indptr[num_seqs] */
+  int32_t max_q;               /* max_b n_b  (decode: 1) */
+  int32_t max_kv;              /* max_b L_b */
+  const int32_t* h_qo_indptr;  /* host copies, optional (NULL = skip host validation) */
+  const int32_t* h_kv_len;
+  const int32_t* h_page_indptr;
+  const int32_t* h_page_ids;
+} mux_batch;
+
+/* a2: write the new tokens' K/V rows into their pool slots of `layer` (bit-exact copy).
+ * k_new, v_new: device bf16 [total_q][Hkv][d]; row qo_indptr[b]+i -> position L_b-n_b+i. */
+int mux_append_kv(mux_pool_t pool, int32_t layer, const mux_batch* batch,
+                  const void* k_new, const void* v_new, mux_stream_t stream);
+
+/* a3: prefill causal attention with cached-prefix pages (tcgen05 + TMEM + TMA kernel).
+ * q: device bf16 [total_q][Hq][d]; o: device [total_q][Hq][d] of o_dtype;
+ * lse: device f32 [total_q][Hq] natural-log LSE, or NULL.  scale: softmax scale (1/sqrt(d)
+ * in the paper's models; passed explicitly, R1).  GQA: q head h uses kv head
+ * h / (Hq/Hkv) (R2).  Hq = num_q_heads. */
+int mux_prefill_attn(mux_pool_t pool, int32_t layer, const mux_batch* batch, int32_t num_q_heads,
+                     const void* q, void* o, int32_t o_dtype, float* lse, float scale,
+                     mux_stream_t stream);
+
+/* a4 + a5: decode split-KV paged attention followed (num_splits > 1) by the
+ * log-sum-exp split combine.  q: device bf16 [num_seqs][Hq][d]; o, lse as prefill.
+ * num_splits: 0 = auto (mux_decode_num_splits for this device's SM count).
+ * ws: device workspace of >= mux_decode_workspace_bytes(num_seqs, Hq, d, num_splits)
+ * bytes (may be NULL when the resolved num_splits is 1). */
+int mux_decode_attn(mux_pool_t pool, int32_t layer, const mux_batch* batch, int32_t num_q_heads,
+                    const void* q, void* o, int32_t o_dtype, float* lse, float scale,
+                    int32_t num_splits, void* ws, size_t ws_bytes, mux_stream_t stream);
+size_t mux_decode_workspace_bytes(int32_t num_seqs, int32_t num_q_heads, int32_t head_dim,
+                                  int32_t num_splits);
+/* host heuristic: splits so that num_seqs*Hkv*splits CTAs fill `num_sms` SMs, capped by
+ * the pages of the longest sequence */
+int32_t mux_decode_num_splits(int32_t num_seqs, int32_t num_kv_heads, int32_t max_kv, int32_t num_sms);
+
+/* ------------------------------------------------------------------------------------
+ * SM partitions (a6).  P:473: GreenContext binds streams to SM sets, reconfiguration
+ * costs a stream synchronisation; 16-SM granularity.  For every requested
+ * decode SM count k the library splits the device's SMs ONCE, disjointly, into
+ * {k decode SMs, remainder prefill SMs} (cuDevSmResourceSplitByCount) and creates one
+ * green context + one stream per side.  Split index -1 means "no partition": two plain
+ * streams on the whole GPU.
+ * ---------------------------------------------------------------------------------- */
+/* rule of SPEC S:303-310 extended to any SM count: decode = k*granularity (k >= 1) while
+ * total - decode >= min_side, ascending.  Writes up to cap values, returns the count
+ * (108 SMs -> 6 configs, 132 -> 7; 148 -> 8) or -MUX_ERR_NO_CONFIG. */
+int32_t mux_partition_configs(int32_t total_sms, int32_t granularity, int32_t min_side,
+                              int32_t* out, int32_t cap);
+/* N_PL = ceil(T_d * N_T / T_P), clamped to [1, remaining] (0 if remaining == 0). */
+int32_t mux_num_prefill_layers(double t_decode, double t_prefill, int32_t n_layers_model,
+                               int32_t remaining);
+
+int mux_partition_create(mux_part_t* out, int32_t device, const int32_t* decode_sms, int32_t n_splits);
+int mux_partition_destroy(mux_part_t part);
+/* granted SM counts (exact, from the driver) and the two streams of split `idx` */
+int mux_partition_query(mux_part_t part, int32_t idx, int32_t* dec_sms, int32_t* pf_sms,
+                        mux_stream_t* dec_stream, mux_stream_t* pf_stream);
+int32_t mux_partition_count(mux_part_t part);
+/* device memory (bytes) taken by creating the partition's green contexts/streams */
+int mux_partition_memory(mux_part_t part, int64_t* bytes);
+int32_t mux_device_sm_count(int32_t device);
+
+/* One side of a mux_run_layer call.  For layer i in [0, num_layers) the side processes
+ * pool layer (layer0 + i) % pool_layers with inputs at base + i*stride (bytes; stride 0
+ * = the same buffer every layer). */
+typedef struct {
+  const mux_batch* batch;
+  int32_t num_q_heads;
+  const void* q;           /* bf16 [total_q][Hq][d] */
+  const void* k_new;       /* bf16 [total_q][Hkv][d]; ignored when append == 0 */
+  const void* v_new;
+  void* o;                 /* [total_q][Hq][d] of o_dtype */
+  float* lse;              /* [total_q][Hq] or NULL */
+  int64_t q_stride, kv_stride, o_stride, lse_stride;
+  int32_t o_dtype;
+  float scale;
+  int32_t layer0, num_layers;
+  int32_t append;          /* 1: mux_append_kv before the attention of every layer */
+  int32_t num_splits;      /* decode only; 0 = auto for the decode partition's SM count */
+  void* ws;                /* decode only */
+  size_t ws_bytes;
+} mux_side;
+
+/* device timestamps (%globaltimer, ns) written by 1-thread stamp kernels on each side */
+typedef struct {
+  uint64_t dec_start_ns, dec_end_ns, pf_start_ns, pf_end_ns;
+} mux_side_times;
+
+/* a6: co-execute decode (a2+a4+a5 per layer, enqueued FIRST) on the decode SM set
+ * and prefill (a2+a3 per layer, layer-wise P:529) on the prefill SM set of split
+ * `split_idx`.  Either side may be NULL (that side does not run: isolated mode, so iso and
+ * mux timings come from the same call).  Ordering: both side streams wait for the work
+ * already enqueued on join_stream; join_stream then waits for both sides.  times: device
+ * buffer (or NULL) filled asynchronously; read it after synchronising join_stream. */
+int mux_run_layer(mux_part_t part, int32_t split_idx, mux_pool_t pool,
+                  const mux_side* prefill, const mux_side* decode,
+                  mux_side_times* times, mux_stream_t join_stream);
+
+/* a7 building block (multi-GPU out-projection partial sums, P:702 TP): Y[T][N] (bf16 or
+ * f32) = X[T][K] (bf16, row-major) . W[K][N] (bf16, row-major), fp32 accumulation. */
+int mux_outproj(const void* x, const void* w, void* y, int32_t y_dtype, int32_t T, int32_t K,
+                int32_t N, mux_stream_t stream);
+
+const char* mux_last_error(void);
+/* library version string, e.g. "mux-b200 0.1 sm_100a" */
+const char* mux_version(void);
+
+#if defined(__GNUC__)
+#pragma GCC visibility pop
+#endif
+#ifdef __cplusplus
+}
+#endif
+#endif /* MUX_H_ */

@@ -1,0 +1,13 @@
+"""paper_2504_14489_b200 — B200-native hot path of MuxWise (arXiv 2504.14489).
+
+Thin ctypes binding over the C-ABI library libmux.so (include/mux.h).  Every step of the
+path runs in libmux's CUDA kernels; this module only marshals arguments.  PyTorch is used
+for device memory and streams.  There is NO CPU fallback: if libmux.so is missing or
+cannot be loaded, importing the binding raises.
+"""
+from .binding import (  # noqa: F401
+    MuxError, Batch, Pool, Partition, lib, last_error,
+    mux_pool_create, mux_append_kv, mux_prefill_attn, mux_decode_attn, mux_decode_workspace_bytes,
+    mux_decode_num_splits, mux_partition_configs, mux_num_prefill_layers, mux_partition_create,
+    mux_run_layer, mux_device_sm_count, MUX_DTYPE_BF16, MUX_DTYPE_F32, SideTimes, make_side,
+)

@@ -1,0 +1,355 @@
+"""ctypes binding of include/mux.h (argument marshalling only).
+
+Names follow the C ABI (mux_pool_create, mux_append_kv, mux_prefill_attn, mux_decode_attn,
+mux_run_layer, ...).  Tensors are torch tensors: data_ptr() is passed as a plain pointer.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+from typing import List, Optional, Sequence
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+_SO = os.path.join(_HERE, "libmux.so")
+
+MUX_OK = 0
+MUX_DTYPE_BF16 = 0
+MUX_DTYPE_F32 = 1
+STATUS = {0: "MUX_OK", 1: "MUX_ERR_INVALID_ARG", 2: "MUX_ERR_UNSUPPORTED", 3: "MUX_ERR_POOL_EXHAUSTED",
+          4: "MUX_ERR_SHARED_PAGE_WRITE", 5: "MUX_ERR_NO_CONFIG", 6: "MUX_ERR_CUDA", 7: "MUX_ERR_WORKSPACE"}
+
+c_i32, c_i64, c_u64, c_p, c_f32, c_dbl, c_sz = (ctypes.c_int32, ctypes.c_int64, ctypes.c_uint64, ctypes.c_void_p,
+                                                ctypes.c_float, ctypes.c_double, ctypes.c_size_t)
+
+
+class MuxError(RuntimeError):
+    def __init__(self, code: int, msg: str):
+        super().__init__(f"{STATUS.get(code, code)}: {msg}")
+        self.code = code
+
+
+class PoolDesc(ctypes.Structure):
+    _fields_ = [("num_layers", c_i32), ("num_pages", c_i32), ("page_size", c_i32), ("num_kv_heads", c_i32),
+                ("head_dim", c_i32), ("k_storage", c_p), ("v_storage", c_p), ("free_list_seed", c_u64)]
+
+
+class BatchC(ctypes.Structure):
+    _fields_ = [("num_seqs", c_i32), ("qo_indptr", c_p), ("kv_len", c_p), ("page_indptr", c_p),
+                ("page_ids", c_p), ("total_q", c_i32), ("max_q", c_i32), ("max_kv", c_i32),
+                ("h_qo_indptr", c_p), ("h_kv_len", c_p), ("h_page_indptr", c_p), ("h_page_ids", c_p)]
+
+
+class SideC(ctypes.Structure):
+    _fields_ = [("batch", ctypes.POINTER(BatchC)), ("num_q_heads", c_i32), ("q", c_p), ("k_new", c_p),
+                ("v_new", c_p), ("o", c_p), ("lse", c_p), ("q_stride", c_i64), ("kv_stride", c_i64),
+                ("o_stride", c_i64), ("lse_stride", c_i64), ("o_dtype", c_i32), ("scale", c_f32),
+                ("layer0", c_i32), ("num_layers", c_i32), ("append", c_i32), ("num_splits", c_i32),
+                ("ws", c_p), ("ws_bytes", c_sz)]
+
+
+class SideTimes(ctypes.Structure):
+    _fields_ = [("dec_start_ns", c_u64), ("dec_end_ns", c_u64), ("pf_start_ns", c_u64), ("pf_end_ns", c_u64)]
+
+
+_lib = None
+
+
+def lib():
+    """Load libmux.so (in-tree).  Raises if it is missing: there is no fallback path."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(_SO):
+        raise ImportError(f"libmux.so not built ({_SO}); run __graft_entry__.build()")
+    L = ctypes.CDLL(_SO)
+    sig = {
+        "mux_pool_create": [ctypes.POINTER(c_p), ctypes.POINTER(PoolDesc)],
+        "mux_pool_destroy": [c_p],
+        "mux_pool_alloc_pages": [c_p, c_i32, c_p],
+        "mux_pool_share_pages": [c_p, c_i32, c_p],
+        "mux_pool_free_pages": [c_p, c_i32, c_p],
+        "mux_pool_num_free": [c_p, ctypes.POINTER(c_i32)],
+        "mux_pool_refcount": [c_p, c_i32, ctypes.POINTER(c_i32)],
+        "mux_pool_free_list": [c_p, c_p, c_i32, ctypes.POINTER(c_i32)],
+        "mux_pool_storage": [c_p, ctypes.POINTER(c_p), ctypes.POINTER(c_p)],
+        "mux_append_kv": [c_p, c_i32, ctypes.POINTER(BatchC), c_p, c_p, c_p],
+        "mux_prefill_attn": [c_p, c_i32, ctypes.POINTER(BatchC), c_i32, c_p, c_p, c_i32, c_p, c_f32, c_p],
+        "mux_decode_attn": [c_p, c_i32, ctypes.POINTER(BatchC), c_i32, c_p, c_p, c_i32, c_p, c_f32, c_i32, c_p,
+                            c_sz, c_p],
+        "mux_partition_create": [ctypes.POINTER(c_p), c_i32, c_p, c_i32],
+        "mux_partition_destroy": [c_p],
+        "mux_partition_query": [c_p, c_i32, ctypes.POINTER(c_i32), ctypes.POINTER(c_i32), ctypes.POINTER(c_p),
+                                ctypes.POINTER(c_p)],
+        "mux_partition_memory": [c_p, ctypes.POINTER(c_i64)],
+        "mux_run_layer": [c_p, c_i32, c_p, ctypes.POINTER(SideC), ctypes.POINTER(SideC), c_p, c_p],
+        "mux_outproj": [c_p, c_p, c_p, c_i32, c_i32, c_i32, c_i32, c_p],
+    }
+    for name, args in sig.items():
+        f = getattr(L, name)
+        f.argtypes = args
+        f.restype = ctypes.c_int
+    L.mux_decode_workspace_bytes.argtypes = [c_i32, c_i32, c_i32, c_i32]
+    L.mux_decode_workspace_bytes.restype = c_sz
+    L.mux_decode_num_splits.argtypes = [c_i32, c_i32, c_i32, c_i32]
+    L.mux_decode_num_splits.restype = c_i32
+    L.mux_partition_configs.argtypes = [c_i32, c_i32, c_i32, c_p, c_i32]
+    L.mux_partition_configs.restype = c_i32
+    L.mux_num_prefill_layers.argtypes = [c_dbl, c_dbl, c_i32, c_i32]
+    L.mux_num_prefill_layers.restype = c_i32
+    L.mux_partition_count.argtypes = [c_p]
+    L.mux_partition_count.restype = c_i32
+    L.mux_device_sm_count.argtypes = [c_i32]
+    L.mux_device_sm_count.restype = c_i32
+    L.mux_last_error.restype = ctypes.c_char_p
+    L.mux_version.restype = ctypes.c_char_p
+    _lib = L
+    return L
+
+
+def last_error() -> str:
+    return lib().mux_last_error().decode()
+
+
+def _check(rc: int):
+    if rc != MUX_OK:
+        raise MuxError(rc, last_error())
+
+
+def _ptr(t) -> Optional[int]:
+    if t is None:
+        return None
+    return t.data_ptr()
+
+
+def _stream(stream) -> Optional[int]:
+    import torch
+    if stream is None:
+        return torch.cuda.current_stream().cuda_stream
+    if isinstance(stream, int):
+        return stream
+    return stream.cuda_stream
+
+
+def _np32(a) -> np.ndarray:
+    return np.ascontiguousarray(np.asarray(a, dtype=np.int32))
+
+
+# ------------------------------------------------------------------------------ pool
+class Pool:
+    """A paged KV pool (a1).  Storage: torch bf16 tensors [layers, pages, Hkv, 16, d] passed
+    to the library (or library-owned when k/v are None)."""
+
+    def __init__(self, num_layers: int, num_pages: int, num_kv_heads: int, head_dim: int, seed: int,
+                 k=None, v=None, device_ptrs: Optional[tuple] = None):
+        self.desc = PoolDesc(num_layers, num_pages, 16, num_kv_heads, head_dim, None, None, seed)
+        if k is not None:
+            self.desc.k_storage, self.desc.v_storage = _ptr(k), _ptr(v)
+        elif device_ptrs is not None:
+            self.desc.k_storage, self.desc.v_storage = device_ptrs
+        self.k, self.v = k, v
+        h = c_p()
+        _check(lib().mux_pool_create(ctypes.byref(h), ctypes.byref(self.desc)))
+        self.h = h
+
+    def close(self):
+        if self.h:
+            lib().mux_pool_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def alloc(self, n: int) -> List[int]:
+        out = np.zeros(max(n, 1), np.int32)
+        _check(lib().mux_pool_alloc_pages(self.h, n, out.ctypes.data))
+        return [int(x) for x in out[:n]]
+
+    def share(self, ids: Sequence[int]):
+        a = _np32(ids)
+        _check(lib().mux_pool_share_pages(self.h, len(a), a.ctypes.data))
+
+    def free(self, ids: Sequence[int]):
+        a = _np32(ids)
+        _check(lib().mux_pool_free_pages(self.h, len(a), a.ctypes.data))
+
+    def num_free(self) -> int:
+        n = c_i32()
+        _check(lib().mux_pool_num_free(self.h, ctypes.byref(n)))
+        return n.value
+
+    def refcount(self, page: int) -> int:
+        n = c_i32()
+        _check(lib().mux_pool_refcount(self.h, page, ctypes.byref(n)))
+        return n.value
+
+    def free_list(self) -> List[int]:
+        n = c_i32()
+        _check(lib().mux_pool_free_list(self.h, None, 0, ctypes.byref(n)))
+        out = np.zeros(max(1, n.value), np.int32)
+        _check(lib().mux_pool_free_list(self.h, out.ctypes.data, n.value, ctypes.byref(n)))
+        return [int(x) for x in out[:n.value]]
+
+    def page_tables(self, pages_needed: Sequence[int]):
+        ind, ids = [0], []
+        for n in pages_needed:
+            ids.extend(self.alloc(n))
+            ind.append(len(ids))
+        return ind, ids
+
+
+def mux_pool_create(num_layers, num_pages, num_kv_heads, head_dim, seed, k=None, v=None) -> Pool:
+    return Pool(num_layers, num_pages, num_kv_heads, head_dim, seed, k, v)
+
+
+# ------------------------------------------------------------------------------ batch
+class Batch:
+    """Batch descriptor (device CSR arrays as torch int32 tensors + host copies for validation)."""
+
+    def __init__(self, qo_indptr, kv_len, page_indptr, page_ids, device="cuda", host_check: bool = True):
+        import torch
+        self.h_qo = _np32(qo_indptr)
+        self.h_kv = _np32(kv_len)
+        self.h_pind = _np32(page_indptr)
+        self.h_pids = _np32(page_ids) if len(page_ids) else np.zeros(1, np.int32)
+        self.num_seqs = len(self.h_kv)
+        self.total_q = int(self.h_qo[-1])
+        n = np.diff(self.h_qo)
+        self.max_q = int(n.max())
+        self.max_kv = int(self.h_kv.max())
+        self.d_qo = torch.from_numpy(self.h_qo).to(device)
+        self.d_kv = torch.from_numpy(self.h_kv).to(device)
+        self.d_pind = torch.from_numpy(self.h_pind).to(device)
+        self.d_pids = torch.from_numpy(self.h_pids).to(device)
+        self.c = BatchC(self.num_seqs, _ptr(self.d_qo), _ptr(self.d_kv), _ptr(self.d_pind), _ptr(self.d_pids),
+                        self.total_q, self.max_q, self.max_kv,
+                        self.h_qo.ctypes.data if host_check else None, self.h_kv.ctypes.data if host_check else None,
+                        self.h_pind.ctypes.data if host_check else None,
+                        self.h_pids.ctypes.data if host_check else None)
+
+    @property
+    def ref(self):
+        return ctypes.byref(self.c)
+
+
+def mux_append_kv(pool: Pool, layer: int, batch: Batch, k_new, v_new, stream=None):
+    _check(lib().mux_append_kv(pool.h, layer, batch.ref, _ptr(k_new), _ptr(v_new), _stream(stream)))
+
+
+def mux_prefill_attn(pool: Pool, layer: int, batch: Batch, num_q_heads: int, q, o, lse=None,
+                     scale: Optional[float] = None, stream=None):
+    import torch
+    scale = scale if scale is not None else 1.0 / float(np.sqrt(pool.desc.head_dim))
+    od = MUX_DTYPE_F32 if o.dtype == torch.float32 else MUX_DTYPE_BF16
+    _check(lib().mux_prefill_attn(pool.h, layer, batch.ref, num_q_heads, _ptr(q), _ptr(o), od, _ptr(lse),
+                                  scale, _stream(stream)))
+
+
+def mux_decode_attn(pool: Pool, layer: int, batch: Batch, num_q_heads: int, q, o, lse=None,
+                    scale: Optional[float] = None, num_splits: int = 0, ws=None, stream=None):
+    import torch
+    scale = scale if scale is not None else 1.0 / float(np.sqrt(pool.desc.head_dim))
+    od = MUX_DTYPE_F32 if o.dtype == torch.float32 else MUX_DTYPE_BF16
+    ws_bytes = ws.numel() * ws.element_size() if ws is not None else 0
+    _check(lib().mux_decode_attn(pool.h, layer, batch.ref, num_q_heads, _ptr(q), _ptr(o), od, _ptr(lse), scale,
+                                 num_splits, _ptr(ws), ws_bytes, _stream(stream)))
+
+
+def mux_decode_workspace_bytes(num_seqs: int, num_q_heads: int, head_dim: int, num_splits: int) -> int:
+    return int(lib().mux_decode_workspace_bytes(num_seqs, num_q_heads, head_dim, num_splits))
+
+
+def mux_decode_num_splits(num_seqs: int, num_kv_heads: int, max_kv: int, num_sms: int) -> int:
+    return int(lib().mux_decode_num_splits(num_seqs, num_kv_heads, max_kv, num_sms))
+
+
+def mux_partition_configs(total_sms: int, granularity: int = 16, min_side: int = 12) -> List[int]:
+    n = lib().mux_partition_configs(total_sms, granularity, min_side, None, 0)
+    if n < 0:
+        raise MuxError(-n, last_error())
+    out = np.zeros(n, np.int32)
+    lib().mux_partition_configs(total_sms, granularity, min_side, out.ctypes.data, n)
+    return [int(x) for x in out]
+
+
+def mux_num_prefill_layers(t_decode: float, t_prefill: float, n_layers_model: int, remaining: int) -> int:
+    return int(lib().mux_num_prefill_layers(t_decode, t_prefill, n_layers_model, remaining))
+
+
+def mux_device_sm_count(device: int = 0) -> int:
+    return int(lib().mux_device_sm_count(device))
+
+
+# ------------------------------------------------------------------------------ partitions
+class Partition:
+    def __init__(self, device: int, decode_sms: Sequence[int]):
+        a = _np32(decode_sms) if len(decode_sms) else np.zeros(1, np.int32)
+        h = c_p()
+        _check(lib().mux_partition_create(ctypes.byref(h), device, a.ctypes.data, len(decode_sms)))
+        self.h = h
+        self.n = len(decode_sms)
+
+    def query(self, idx: int):
+        d, p, sd, sp = c_i32(), c_i32(), c_p(), c_p()
+        _check(lib().mux_partition_query(self.h, idx, ctypes.byref(d), ctypes.byref(p), ctypes.byref(sd),
+                                         ctypes.byref(sp)))
+        return d.value, p.value, sd.value, sp.value
+
+    def memory_bytes(self) -> int:
+        b = c_i64()
+        _check(lib().mux_partition_memory(self.h, ctypes.byref(b)))
+        return b.value
+
+    def close(self):
+        if self.h:
+            lib().mux_partition_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def mux_partition_create(device: int, decode_sms: Sequence[int]) -> Partition:
+    return Partition(device, decode_sms)
+
+
+def make_side(batch: Batch, num_q_heads: int, q, o, k_new=None, v_new=None, lse=None, scale: float = 1.0,
+              layer0: int = 0, num_layers: int = 1, append: bool = False, num_splits: int = 0, ws=None,
+              per_layer_inputs: bool = False) -> SideC:
+    """Build a mux_side.  per_layer_inputs: q/k_new/v_new/o/lse carry a leading layer dim
+    and layer i uses slice i (stride = one slice); otherwise every layer reuses the buffers."""
+    import torch
+
+    def stride(t):
+        if t is None or not per_layer_inputs:
+            return 0
+        return t[0].numel() * t.element_size()
+
+    s = SideC()
+    s.batch = ctypes.pointer(batch.c)
+    s.num_q_heads = num_q_heads
+    s.q, s.k_new, s.v_new, s.o, s.lse = _ptr(q), _ptr(k_new), _ptr(v_new), _ptr(o), _ptr(lse)
+    s.q_stride, s.kv_stride, s.o_stride, s.lse_stride = stride(q), stride(k_new), stride(o), stride(lse)
+    s.o_dtype = MUX_DTYPE_F32 if o.dtype == torch.float32 else MUX_DTYPE_BF16
+    s.scale = scale
+    s.layer0, s.num_layers = layer0, num_layers
+    s.append = 1 if append else 0
+    s.num_splits = num_splits
+    s.ws = _ptr(ws)
+    s.ws_bytes = ws.numel() * ws.element_size() if ws is not None else 0
+    s._keep = (batch, q, o, k_new, v_new, lse, ws)
+    return s
+
+
+def mux_run_layer(part: Partition, split_idx: int, pool: Pool, prefill: Optional[SideC], decode: Optional[SideC],
+                  times=None, join_stream=None):
+    _check(lib().mux_run_layer(part.h, split_idx, pool.h, ctypes.byref(prefill) if prefill is not None else None,
+                               ctypes.byref(decode) if decode is not None else None, _ptr(times),
+                               _stream(join_stream)))

@@ -1,0 +1,428 @@
+// a4 decode split-KV paged attention + a5 log-sum-exp split combine.
+//
+// PAPER: decode attends one new token over r+1 cached keys, O(d^2 + (r+1)d) (Table 2,
+// P:590), memory-intensive, latency linear in sum r (Eq.2).  The split-KV
+// (flash-decoding) organisation + combine pass is BASELINE.json's north_star; it is an
+// exact reorganisation of the softmax.
+//
+// B200 design: HBM-bound, so the kernel is a page-streaming engine.
+//   grid (num_splits, Hkv, B), 5 warps: warp 4 = producer, warps 0-3 = consumers.
+//   Producer: one elected lane issues TMA (cp.async.bulk.tensor, SWIZZLE_128B) for the K
+//   and V blocks of one 16-token page (2 x d x 16 bf16 = 8 KiB at d=128) into a STAGES-deep
+//   mbarrier ring (96 KiB in flight per CTA, 2 CTAs/SM).  Page ids are prefetched 32 at a
+//   time with one coalesced warp load.
+//   Consumers: page i is processed by warp i%4 with the legacy tensor pipe (the group of
+//   g <= 8 q heads is the N=8 side, so FP32 ALU is left for the softmax):
+//     S^T[16 tok x 8 heads] = K_page[16 x d] . Q^T      (mma.m16n8k16, A = K via ldmatrix)
+//     online softmax per head column (warp shuffles over the 8 token lanes)
+//     P^T -> B fragments with movmatrix.trans (no smem round trip)
+//     O^T[d x 8] += V_page^T . P^T                      (A = V^T via ldmatrix.trans)
+//   Warps merge their (m, l, O) states in smem at the end; with one split the CTA writes
+//   the normalised output, otherwise fp32 partials (o, m, l) for the combine kernel.
+#include <math.h>
+
+#include "pool.h"
+
+namespace mux {
+namespace {
+
+constexpr int kConsumerWarps = 4;
+constexpr int kDecodeThreads = (kConsumerWarps + 1) * 32;
+
+struct DecodeParams {
+  const uint16_t* q;         // [B][Hq][D]
+  void* o;                   // [B][Hq][D]
+  float* lse;                // [B][Hq] or null
+  float* part_o;             // [B][Hq][S][D]
+  float* part_m;             // [B][Hq][S]  (log2 domain)
+  float* part_l;             // [B][Hq][S]
+  const int32_t* kv_len;
+  const int32_t* page_indptr;
+  const int32_t* page_ids;
+  int num_splits, hq, hkv, g;
+  int page_row0;             // layer * num_pages (TMA dim-3 coordinate offset)
+  int o_f32;
+  float scale_log2;
+};
+
+template <int D, int STAGES>
+struct DecodeSmem {
+  static constexpr int kBoxes = D / 64;                 // 64-dim TMA boxes per page per K or V
+  static constexpr int kPageBytes = D * kPage * 2;      // K (or V) bytes of one (page, kv head)
+  static constexpr int kStageBytes = 2 * kPageBytes;    // K + V
+  static constexpr int kQRows = 16;                     // up to g = 16 heads
+  static constexpr int kQStride = D + 8;                // padded row (bf16) -> conflict-free ldmatrix
+  static constexpr int kStagesOff = 0;
+  static constexpr int kQOff = STAGES * kStageBytes;
+  static constexpr int kBarOff = kQOff + kQRows * kQStride * 2;
+  static constexpr int kPageIdsOff = kBarOff + 2 * STAGES * 8;
+  static constexpr int kBytes = kPageIdsOff + 16;
+  // merge area (aliases the stage ring after the main loop)
+  static constexpr int kMergeO = 0;                                        // [warps][16 heads][D] f32
+  static constexpr int kMergeM = kConsumerWarps * 16 * D * 4;              // [warps][16]
+  static constexpr int kMergeL = kMergeM + kConsumerWarps * 16 * 4;
+  static_assert(kMergeL + kConsumerWarps * 16 * 4 <= STAGES * kStageBytes, "merge area too big");
+};
+
+template <int D, int NT, int STAGES>
+__global__ void __launch_bounds__(kDecodeThreads, 2)
+    decode_kernel(const __grid_constant__ CUtensorMap tmap_k, const __grid_constant__ CUtensorMap tmap_v,
+                  const DecodeParams p) {
+  using L = DecodeSmem<D, STAGES>;
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + L::kBarOff);
+  uint64_t* empty = full + STAGES;
+  uint16_t* qs = reinterpret_cast<uint16_t*>(smem + L::kQOff);
+
+  const int split = blockIdx.x, kvh = blockIdx.y, b = blockIdx.z;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int kv_len = __ldg(p.kv_len + b);
+  const int npages = (kv_len + kPage - 1) / kPage;
+  const int pps = (npages + p.num_splits - 1) / p.num_splits;
+  const int pg0 = min(npages, split * pps);
+  const int pg1 = min(npages, pg0 + pps);
+  const int n_my = pg1 - pg0;
+  const int* ptab = p.page_ids + __ldg(p.page_indptr + b);
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < STAGES; ++s) {
+      dev::mbar_init(&full[s], 1);
+      dev::mbar_init(&empty[s], 1);
+    }
+    dev::fence_mbar_init();
+  }
+  // Q of the g heads sharing kv head `kvh` -> padded smem rows; rows >= g are zero
+  {
+    const uint16_t* qsrc = p.q + (static_cast<size_t>(b) * p.hq + static_cast<size_t>(kvh) * p.g) * D;
+    for (int i = threadIdx.x; i < 8 * NT * (D / 8); i += kDecodeThreads) {
+      const int h = i / (D / 8), c = i % (D / 8);
+      uint4 v = make_uint4(0, 0, 0, 0);
+      if (h < p.g) v = __ldg(reinterpret_cast<const uint4*>(qsrc + static_cast<size_t>(h) * D) + c);
+      *reinterpret_cast<uint4*>(qs + h * L::kQStride + c * 8) = v;
+    }
+  }
+  __syncthreads();
+
+  // per-thread softmax state (heads 2*(lane%4)+{0,1} of each 8-head tile), O^T accumulators
+  float m_run[NT][2], l_run[NT][2];
+  float oacc[D / 16][NT][4];
+#pragma unroll
+  for (int nt = 0; nt < NT; ++nt) {
+    m_run[nt][0] = m_run[nt][1] = -INFINITY;
+    l_run[nt][0] = l_run[nt][1] = 0.f;
+#pragma unroll
+    for (int mt = 0; mt < D / 16; ++mt) oacc[mt][nt][0] = oacc[mt][nt][1] = oacc[mt][nt][2] = oacc[mt][nt][3] = 0.f;
+  }
+
+  if (warp == kConsumerWarps) {
+    // ------------------------------------------------------------ producer
+    if (lane == 0) {
+      dev::tma_prefetch(&tmap_k);
+      dev::tma_prefetch(&tmap_v);
+    }
+    int ids = 0;
+    for (int i = 0; i < n_my; ++i) {
+      if ((i & 31) == 0) ids = (pg0 + i + lane < pg1) ? __ldg(ptab + pg0 + i + lane) : 0;
+      const int page = __shfl_sync(0xffffffffu, ids, i & 31);
+      const int s = i % STAGES;
+      if (lane == 0) {
+        if (i >= STAGES) dev::mbar_wait(&empty[s], ((i / STAGES) - 1) & 1);
+        dev::mbar_expect_tx(&full[s], L::kStageBytes);
+        uint8_t* kdst = smem + L::kStagesOff + s * L::kStageBytes;
+        uint8_t* vdst = kdst + L::kPageBytes;
+#pragma unroll
+        for (int bx = 0; bx < L::kBoxes; ++bx) {
+          dev::tma_load_4d(kdst + bx * 2048, &tmap_k, &full[s], bx * 64, 0, kvh, p.page_row0 + page);
+          dev::tma_load_4d(vdst + bx * 2048, &tmap_v, &full[s], bx * 64, 0, kvh, p.page_row0 + page);
+        }
+      }
+    }
+  } else {
+    // ------------------------------------------------------------ consumers
+    // Q^T B-fragments: b0 = Q[head g][16kc + 2q..], b1 = Q[head g][16kc + 8 + 2q..]
+    uint32_t qf[NT][D / 16][2];
+#pragma unroll
+    for (int nt = 0; nt < NT; ++nt) {
+#pragma unroll
+      for (int kc = 0; kc < D / 16; kc += 2) {
+        const int mi = lane >> 3;                        // matrix: (kc,lo) (kc,hi) (kc+1,lo) (kc+1,hi)
+        const int row = nt * 8 + (lane & 7);
+        const int chunk = 2 * kc + mi;                   // 8-dim chunk
+        dev::ldsm_x4(dev::smem_u32(qs + row * L::kQStride + chunk * 8), qf[nt][kc][0], qf[nt][kc][1],
+                     qf[nt][kc + 1][0], qf[nt][kc + 1][1]);
+      }
+    }
+    const int g4 = lane >> 2, q4 = lane & 3;
+    for (int i = warp; i < n_my; i += kConsumerWarps) {
+      const int s = i % STAGES;
+      dev::mbar_wait(&full[s], (i / STAGES) & 1);
+      uint8_t* kbuf = smem + L::kStagesOff + s * L::kStageBytes;
+      uint8_t* vbuf = kbuf + L::kPageBytes;
+      const int pos0 = (pg0 + i) * kPage;
+      const int valid = min(kPage, kv_len - pos0);
+      if (valid < kPage) {
+        // slots past the sequence end may hold anything (NaN-poisoned in tests): zero V rows
+        // so that P = 0 never meets NaN in the PV MMA; K rows are masked by select below.
+        for (int r = valid; r < kPage; ++r)
+          for (int c = lane; c < L::kBoxes * 8; c += 32)
+            *reinterpret_cast<uint4*>(vbuf + (c >> 3) * 2048 + r * 128 + (c & 7) * 16) = make_uint4(0, 0, 0, 0);
+        __syncwarp();
+      }
+      // ---- S^T = K . Q^T
+      float sacc[NT][4];
+#pragma unroll
+      for (int nt = 0; nt < NT; ++nt) sacc[nt][0] = sacc[nt][1] = sacc[nt][2] = sacc[nt][3] = 0.f;
+      const uint32_t kbase = dev::smem_u32(kbuf);
+#pragma unroll
+      for (int kc = 0; kc < D / 16; ++kc) {
+        const int mi = lane >> 3;
+        const int tok = (lane & 7) + ((mi & 1) << 3);
+        const int chunk = 2 * kc + (mi >> 1);
+        uint32_t a0, a1, a2, a3;
+        dev::ldsm_x4(kbase + (chunk >> 3) * 2048 + dev::sw128(tok, chunk & 7), a0, a1, a2, a3);
+#pragma unroll
+        for (int nt = 0; nt < NT; ++nt) dev::mma_bf16_16816(sacc[nt], a0, a1, a2, a3, qf[nt][kc][0], qf[nt][kc][1]);
+      }
+      // ---- online softmax (log2 domain); thread holds tokens g4, g4+8 x heads 2q4, 2q4+1
+      const bool v0 = g4 < valid, v1 = (g4 + 8) < valid;
+      uint32_t pb[NT][2];
+      float alpha[NT][2];
+#pragma unroll
+      for (int nt = 0; nt < NT; ++nt) {
+        float x[4];
+        x[0] = v0 ? sacc[nt][0] * p.scale_log2 : -INFINITY;
+        x[1] = v0 ? sacc[nt][1] * p.scale_log2 : -INFINITY;
+        x[2] = v1 ? sacc[nt][2] * p.scale_log2 : -INFINITY;
+        x[3] = v1 ? sacc[nt][3] * p.scale_log2 : -INFINITY;
+        float mx0 = fmaxf(x[0], x[2]), mx1 = fmaxf(x[1], x[3]);
+#pragma unroll
+        for (int off = 4; off < 32; off <<= 1) {
+          mx0 = fmaxf(mx0, __shfl_xor_sync(0xffffffffu, mx0, off));
+          mx1 = fmaxf(mx1, __shfl_xor_sync(0xffffffffu, mx1, off));
+        }
+        const float mn0 = fmaxf(m_run[nt][0], mx0), mn1 = fmaxf(m_run[nt][1], mx1);  // finite: valid >= 1
+        alpha[nt][0] = dev::ex2(m_run[nt][0] - mn0);
+        alpha[nt][1] = dev::ex2(m_run[nt][1] - mn1);
+        m_run[nt][0] = mn0;
+        m_run[nt][1] = mn1;
+        const float p0 = dev::ex2(x[0] - mn0), p1 = dev::ex2(x[1] - mn1);
+        const float p2 = dev::ex2(x[2] - mn0), p3 = dev::ex2(x[3] - mn1);
+        l_run[nt][0] = l_run[nt][0] * alpha[nt][0] + p0 + p2;
+        l_run[nt][1] = l_run[nt][1] * alpha[nt][1] + p1 + p3;
+        pb[nt][0] = dev::movmatrix_t(dev::pack_bf16(p0, p1));   // tokens 0-7  -> b0
+        pb[nt][1] = dev::movmatrix_t(dev::pack_bf16(p2, p3));   // tokens 8-15 -> b1
+      }
+      // ---- O^T = alpha * O^T + V^T . P^T
+      const uint32_t vbase = dev::smem_u32(vbuf);
+#pragma unroll
+      for (int mt = 0; mt < D / 16; ++mt) {
+        const int mi = lane >> 3;
+        const int tok = (lane & 7) + ((mi >> 1) << 3);
+        const int chunk = 2 * mt + (mi & 1);
+        uint32_t a0, a1, a2, a3;
+        dev::ldsm_x4_t(vbase + (chunk >> 3) * 2048 + dev::sw128(tok, chunk & 7), a0, a1, a2, a3);
+#pragma unroll
+        for (int nt = 0; nt < NT; ++nt) {
+          oacc[mt][nt][0] *= alpha[nt][0];
+          oacc[mt][nt][1] *= alpha[nt][1];
+          oacc[mt][nt][2] *= alpha[nt][0];
+          oacc[mt][nt][3] *= alpha[nt][1];
+          dev::mma_bf16_16816(oacc[mt][nt], a0, a1, a2, a3, pb[nt][0], pb[nt][1]);
+        }
+      }
+      __syncwarp();
+      if (lane == 0) dev::mbar_arrive(&empty[s]);
+    }
+    // finish row sums over the 8 token lanes
+#pragma unroll
+    for (int nt = 0; nt < NT; ++nt)
+#pragma unroll
+      for (int off = 4; off < 32; off <<= 1) {
+        l_run[nt][0] += __shfl_xor_sync(0xffffffffu, l_run[nt][0], off);
+        l_run[nt][1] += __shfl_xor_sync(0xffffffffu, l_run[nt][1], off);
+      }
+  }
+  __syncthreads();  // all TMA traffic consumed: the stage ring becomes the merge area
+
+  float* mo = reinterpret_cast<float*>(smem + L::kMergeO);
+  float* mm = reinterpret_cast<float*>(smem + L::kMergeM);
+  float* ml = reinterpret_cast<float*>(smem + L::kMergeL);
+  if (warp < kConsumerWarps) {
+    const int g4 = lane >> 2, q4 = lane & 3;
+#pragma unroll
+    for (int nt = 0; nt < NT; ++nt) {
+      const int h0 = nt * 8 + 2 * q4;
+      if (g4 == 0) {
+        mm[warp * 16 + h0] = m_run[nt][0];
+        mm[warp * 16 + h0 + 1] = m_run[nt][1];
+        ml[warp * 16 + h0] = l_run[nt][0];
+        ml[warp * 16 + h0 + 1] = l_run[nt][1];
+      }
+#pragma unroll
+      for (int mt = 0; mt < D / 16; ++mt) {
+        float* base = mo + (warp * 16) * D;
+        base[h0 * D + mt * 16 + g4] = oacc[mt][nt][0];
+        base[(h0 + 1) * D + mt * 16 + g4] = oacc[mt][nt][1];
+        base[h0 * D + mt * 16 + g4 + 8] = oacc[mt][nt][2];
+        base[(h0 + 1) * D + mt * 16 + g4 + 8] = oacc[mt][nt][3];
+      }
+    }
+  }
+  __syncthreads();
+  // combine the 4 warp states: element (head, dim) per thread
+  const int heads = p.g;
+  for (int e = threadIdx.x; e < heads * D; e += kDecodeThreads) {
+    const int h = e / D, c = e % D;
+    float M = -INFINITY;
+#pragma unroll
+    for (int w = 0; w < kConsumerWarps; ++w) M = fmaxf(M, mm[w * 16 + h]);
+    float Ls = 0.f, acc = 0.f;
+    if (M != -INFINITY) {
+#pragma unroll
+      for (int w = 0; w < kConsumerWarps; ++w) {
+        const float mw = mm[w * 16 + h];
+        if (mw == -INFINITY) continue;
+        const float sc = dev::ex2(mw - M);
+        Ls += sc * ml[w * 16 + h];
+        acc += sc * mo[(w * 16 + h) * D + c];
+      }
+    }
+    const int qh = kvh * p.g + h;
+    const size_t row = static_cast<size_t>(b) * p.hq + qh;
+    if (p.num_splits == 1) {
+      const float out = acc / Ls;
+      if (p.o_f32) static_cast<float*>(p.o)[row * D + c] = out;
+      else static_cast<__nv_bfloat16*>(p.o)[row * D + c] = __float2bfloat16_rn(out);
+      if (c == 0 && p.lse) p.lse[row] = (M + __log2f(Ls)) * 0.69314718055994531f;
+    } else {
+      const size_t pr = row * p.num_splits + split;
+      p.part_o[pr * D + c] = (Ls > 0.f) ? acc / Ls : 0.f;
+      if (c == 0) {
+        p.part_m[pr] = M;
+        p.part_l[pr] = Ls;
+      }
+    }
+  }
+}
+
+// a5: O = sum_s w_s o_s / sum_s w_s with w_s = l_s 2^(m_s - M); LSE = ln2 (M + log2 sum w_s)
+template <int D>
+__global__ void __launch_bounds__(D) combine_kernel(const float* __restrict__ part_o, const float* __restrict__ part_m,
+                                                    const float* __restrict__ part_l, void* o, float* lse,
+                                                    int num_splits, int o_f32) {
+  const size_t row = blockIdx.x;  // b*Hq + h
+  const int c = threadIdx.x;
+  float M = -INFINITY;
+  for (int s = 0; s < num_splits; ++s) {
+    const float l = part_l[row * num_splits + s];
+    if (l > 0.f) M = fmaxf(M, part_m[row * num_splits + s]);
+  }
+  float W = 0.f, acc = 0.f;
+  for (int s = 0; s < num_splits; ++s) {
+    const float l = part_l[row * num_splits + s];
+    if (!(l > 0.f)) continue;
+    const float w = l * dev::ex2(part_m[row * num_splits + s] - M);
+    W += w;
+    acc += w * part_o[(row * num_splits + s) * D + c];
+  }
+  const float out = acc / W;
+  if (o_f32) static_cast<float*>(o)[row * D + c] = out;
+  else static_cast<__nv_bfloat16*>(o)[row * D + c] = __float2bfloat16_rn(out);
+  if (c == 0 && lse) lse[row] = (M + __log2f(W)) * 0.69314718055994531f;
+}
+
+constexpr int kStages = 12;
+
+template <int D, int NT>
+int launch_decode(mux_pool* pool, const DecodeParams& prm, int B, cudaStream_t st) {
+  using L = DecodeSmem<D, kStages>;
+  auto kern = decode_kernel<D, NT, kStages>;
+  const int smem = L::kBytes + 1024;
+  static bool attr_done = false;
+  if (!attr_done) {
+    MUX_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    attr_done = true;
+  }
+  dim3 grid(prm.num_splits, prm.hkv, B);
+  kern<<<grid, kDecodeThreads, smem, st>>>(pool->tmap_k, pool->tmap_v, prm);
+  MUX_CUDA(cudaGetLastError());
+  if (prm.num_splits > 1) {
+    combine_kernel<D><<<B * prm.hq, D, 0, st>>>(prm.part_o, prm.part_m, prm.part_l, prm.o, prm.lse,
+                                                prm.num_splits, prm.o_f32);
+    MUX_CUDA(cudaGetLastError());
+  }
+  return MUX_OK;
+}
+
+}  // namespace
+}  // namespace mux
+
+using namespace mux;
+
+extern "C" {
+
+size_t mux_decode_workspace_bytes(int32_t num_seqs, int32_t hq, int32_t d, int32_t num_splits) {
+  if (num_splits <= 1) return 0;
+  const size_t rows = static_cast<size_t>(num_seqs) * hq * num_splits;
+  return rows * d * 4 + rows * 8 + 256;
+}
+
+int32_t mux_decode_num_splits(int32_t num_seqs, int32_t hkv, int32_t max_kv, int32_t num_sms) {
+  if (num_seqs < 1 || hkv < 1 || max_kv < 1) return 1;
+  if (num_sms < 1) num_sms = 148;
+  const int64_t ctas = static_cast<int64_t>(num_seqs) * hkv;
+  const int64_t target = static_cast<int64_t>(num_sms) * 2 * 2;   // >= 2 waves of 2 CTAs/SM
+  int64_t s = (target + ctas - 1) / ctas;
+  const int64_t pages = (max_kv + kPage - 1) / kPage;
+  const int64_t cap = pages / 4 > 1 ? pages / 4 : 1;                 // >= 4 pages per split
+  if (s > cap) s = cap;
+  if (s > 64) s = 64;
+  if (s < 1) s = 1;
+  return static_cast<int32_t>(s);
+}
+
+int mux_decode_attn(mux_pool_t pool, int32_t layer, const mux_batch* b, int32_t hq, const void* q, void* o,
+                    int32_t o_dtype, float* lse, float scale, int32_t num_splits, void* ws, size_t ws_bytes,
+                    mux_stream_t stream) {
+  int rc = check_pool_layer(pool, layer);
+  if (rc) return rc;
+  if ((rc = validate_batch(b, true))) return rc;
+  const int d = pool->desc.head_dim, hkv = pool->desc.num_kv_heads;
+  if (hq < 1 || hq % hkv) return fail(MUX_ERR_UNSUPPORTED, "num_q_heads must be a positive multiple of Hkv");
+  const int g = hq / hkv;
+  if (g > 16) return fail(MUX_ERR_UNSUPPORTED, "GQA group size > 16 not supported");
+  if (!q || !o) return fail(MUX_ERR_INVALID_ARG, "q/o NULL");
+  if (o_dtype != MUX_DTYPE_BF16 && o_dtype != MUX_DTYPE_F32) return fail(MUX_ERR_INVALID_ARG, "bad o_dtype");
+  if (reinterpret_cast<uintptr_t>(q) & 15) return fail(MUX_ERR_INVALID_ARG, "q must be 16-byte aligned");
+  if (num_splits <= 0) num_splits = mux_decode_num_splits(b->num_seqs, hkv, b->max_kv, device_sm_count());
+  if (num_splits > 1) {
+    if (!ws || ws_bytes < mux_decode_workspace_bytes(b->num_seqs, hq, d, num_splits))
+      return fail(MUX_ERR_WORKSPACE, "decode workspace missing or too small");
+  }
+  if ((rc = pool_tmaps(pool))) return rc;
+  DecodeParams prm{};
+  prm.q = static_cast<const uint16_t*>(q);
+  prm.o = o;
+  prm.lse = lse;
+  const size_t rows = static_cast<size_t>(b->num_seqs) * hq * num_splits;
+  prm.part_o = static_cast<float*>(ws);
+  prm.part_m = num_splits > 1 ? prm.part_o + rows * d : nullptr;
+  prm.part_l = num_splits > 1 ? prm.part_m + rows : nullptr;
+  prm.kv_len = b->kv_len;
+  prm.page_indptr = b->page_indptr;
+  prm.page_ids = b->page_ids;
+  prm.num_splits = num_splits;
+  prm.hq = hq;
+  prm.hkv = hkv;
+  prm.g = g;
+  prm.page_row0 = layer * pool->desc.num_pages;
+  prm.o_f32 = o_dtype == MUX_DTYPE_F32;
+  prm.scale_log2 = scale * 1.4426950408889634f;
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  if (d == 128) return g <= 8 ? launch_decode<128, 1>(pool, prm, b->num_seqs, st)
+                              : launch_decode<128, 2>(pool, prm, b->num_seqs, st);
+  return g <= 8 ? launch_decode<64, 1>(pool, prm, b->num_seqs, st) : launch_decode<64, 2>(pool, prm, b->num_seqs, st);
+}
+
+}  // extern "C"

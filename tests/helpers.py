@@ -65,3 +65,39 @@ def dense_attention(side: SideData, Hq: int, Hkv: int, d: int, scale: float):
 
 def rel_err(a, b):
     return float(np.max(np.abs(a - b)) / max(1e-300, np.max(np.abs(b))))
+
+
+# ------------------------------------------------------------------------------ GPU side
+def gpu_build_side(mux, side: SideData, num_pages: int, seed: int, Hkv: int, d: int, layers: int = 1,
+                   layer: int = 0, poison=True, pool=None):
+    """Library side of a workload: library pool over torch storage (NaN-poisoned), page
+    tables from the LIBRARY allocator, every row (prefix + new) written with mux_append_kv.
+    Returns dict(pool, batch (prefill/new rows), kimg, vimg (torch), page tables)."""
+    import torch
+    spec = side.spec
+    if pool is None:
+        fill = 0x7FC0 if poison else 0
+        kst = torch.full((layers, num_pages, Hkv, 16, d), fill, dtype=torch.int16, device="cuda").view(torch.bfloat16)
+        vst = torch.full((layers, num_pages, Hkv, 16, d), fill, dtype=torch.int16, device="cuda").view(torch.bfloat16)
+        pool = mux.Pool(layers, num_pages, Hkv, d, seed, kst, vst)
+    pind, pids = pool.page_tables(spec.pages_needed())
+    L = spec.L
+    all_batch = mux.Batch(indptr(L), L, pind, pids)
+    all_k = torch.from_numpy(np.concatenate(side.k_rows, axis=0).view(np.int16)).cuda().view(torch.bfloat16)
+    all_v = torch.from_numpy(np.concatenate(side.v_rows, axis=0).view(np.int16)).cuda().view(torch.bfloat16)
+    mux.mux_append_kv(pool, layer, all_batch, all_k, all_v)
+    batch = mux.Batch(indptr(spec.n), L, pind, pids)
+    q = torch.from_numpy(side.q.view(np.int16)).cuda().view(torch.bfloat16)
+    return dict(pool=pool, batch=batch, q=q, page_indptr=np.array(pind, np.int32),
+                page_ids=np.array(pids, np.int32), kv_len=np.array(L, np.int32), qo_indptr=indptr(spec.n))
+
+
+def check_close(gpu_out, ref, atol=2e-3, rtol=1e-2, what=""):
+    """DESIGN.md R8: |d| <= atol + rtol*|ref| element-wise; for fp32 outputs also max|d| <= atol."""
+    g = np.asarray(gpu_out, dtype=np.float64)
+    diff = np.abs(g - ref)
+    bad = diff > atol + rtol * np.abs(ref)
+    assert not np.isnan(g).any(), f"{what}: NaN in GPU output"
+    assert not bad.any(), (f"{what}: {bad.sum()} elements out of tolerance; max|d|={diff.max():.3e} "
+                           f"at {np.unravel_index(diff.argmax(), diff.shape)}")
+    return float(diff.max())

@@ -1,0 +1,125 @@
+"""GPU tests of a6: green-context SM partitions and mux_run_layer (mux == isolated, bitwise;
+parity with the oracle through the multiplexed path; per-side timestamps)."""
+import math
+
+import numpy as np
+import pytest
+
+import oracle
+from synth import SideSpec, Shapes, make_side
+from tests.helpers import check_close, gpu_build_side, oracle_build_side
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def mux():
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("no GPU")
+    import paper_2504_14489_b200 as m
+    m.lib()
+    return m
+
+
+@pytest.fixture(scope="module")
+def part(mux):
+    p = mux.Partition(0, [16, 32, 64, 128])
+    yield p
+    p.close()
+
+
+def test_partition_grants(mux, part):
+    total = mux.mux_device_sm_count(0)
+    for i, want in enumerate([16, 32, 64, 128]):
+        d, p, sd, sp = part.query(i)
+        assert d >= want and d % 8 == 0
+        assert d + p <= total
+        assert sd and sp and sd != sp
+    d, p, _, _ = part.query(-1)
+    assert d == p == total
+    assert part.memory_bytes() >= 0
+
+
+def _workload(mux, Hq=8, Hkv=2, d=128):
+    import torch
+    pf = make_side(801, Shapes(Hq, Hkv, d, 1), SideSpec([37, 0], [300, 129]), decode=False)
+    dc = make_side(802, Shapes(Hq, Hkv, d, 1), SideSpec([c - 1 for c in (700, 17, 4096)], [1, 1, 1]), decode=True)
+    need = sum(pf.spec.pages_needed()) + sum(dc.spec.pages_needed())
+    kst = torch.full((2, need + 8, Hkv, 16, d), 0x7FC0, dtype=torch.int16, device="cuda").view(torch.bfloat16)
+    vst = kst.clone()
+    pool = mux.Pool(2, need + 8, Hkv, d, 5, kst, vst)
+    g_pf = gpu_build_side(mux, pf, need + 8, 5, Hkv, d, layers=2, pool=pool)
+    g_dc = gpu_build_side(mux, dc, need + 8, 5, Hkv, d, layers=2, pool=pool)
+    return pf, dc, pool, g_pf, g_dc
+
+
+def _sides(mux, pool, g_pf, g_dc, Hq, d, pf_T, dc_B, ns=2):
+    import torch
+    o_pf = torch.zeros((pf_T, Hq, d), dtype=torch.float32, device="cuda")
+    o_dc = torch.zeros((dc_B, Hq, d), dtype=torch.float32, device="cuda")
+    wsb = mux.mux_decode_workspace_bytes(dc_B, Hq, d, ns)
+    ws = torch.empty(max(16, wsb), dtype=torch.uint8, device="cuda")
+    s_pf = mux.make_side(g_pf["batch"], Hq, g_pf["q"], o_pf, scale=1 / math.sqrt(d))
+    s_dc = mux.make_side(g_dc["batch"], Hq, g_dc["q"], o_dc, scale=1 / math.sqrt(d), num_splits=ns, ws=ws)
+    return s_pf, s_dc, o_pf, o_dc
+
+
+def test_mux_equals_isolated_bitwise_and_matches_oracle(mux, part):
+    import torch
+    Hq, Hkv, d = 8, 2, 128
+    pf, dc, pool, g_pf, g_dc = _workload(mux, Hq, Hkv, d)
+    times = torch.zeros(4, dtype=torch.int64, device="cuda")
+    for split in (-1, 0, 1, 2, 3):
+        s_pf, s_dc, o_pf, o_dc = _sides(mux, pool, g_pf, g_dc, Hq, d, 429, 3)
+        mux.mux_run_layer(part, split, pool, s_pf, s_dc, times)
+        torch.cuda.synchronize()
+        t = times.cpu().numpy()
+        assert t[1] >= t[0] > 0 and t[3] >= t[2] > 0
+        both_pf, both_dc = o_pf.cpu().numpy(), o_dc.cpu().numpy()
+        s_pf, s_dc, o_pf, o_dc = _sides(mux, pool, g_pf, g_dc, Hq, d, 429, 3)
+        mux.mux_run_layer(part, split, pool, s_pf, None, None)
+        mux.mux_run_layer(part, split, pool, None, s_dc, None)
+        torch.cuda.synchronize()
+        np.testing.assert_array_equal(both_pf, o_pf.cpu().numpy())
+        np.testing.assert_array_equal(both_dc, o_dc.cpu().numpy())
+    # and the multiplexed outputs match the oracle
+    kimg = pool.k[0].view(torch.int16).cpu().numpy().view(np.uint16)
+    vimg = pool.v[0].view(torch.int16).cpu().numpy().view(np.uint16)
+    for side, g, out in ((pf, g_pf, both_pf), (dc, g_dc, both_dc)):
+        ref, _ = oracle.attention(side.q, kimg, vimg, g["qo_indptr"], g["kv_len"], g["page_indptr"],
+                                  g["page_ids"], 1 / math.sqrt(d))
+        check_close(out, ref, what="mux output vs oracle")
+
+
+def test_run_layer_multi_layer_with_append(mux, part):
+    """Layer-wise prefill over 2 pool layers with append on both sides."""
+    import torch
+    Hq, Hkv, d = 4, 1, 64
+    pf = make_side(803, Shapes(Hq, Hkv, d, 1), SideSpec([64], [128]), decode=False)
+    need = sum(pf.spec.pages_needed())
+    kst = torch.full((2, need + 4, Hkv, 16, d), 0x7FC0, dtype=torch.int16, device="cuda").view(torch.bfloat16)
+    pool = mux.Pool(2, need + 4, Hkv, d, 9, kst, kst.clone())
+    pind, pids = pool.page_tables(pf.spec.pages_needed())
+    from synth import indptr
+    L = pf.spec.L
+    # prefix rows go in through append on both layers; the new rows are appended by run_layer
+    pre = mux.Batch(indptr(pf.spec.r), pf.spec.r, [0, 4], pids[:4])
+    kpre = torch.from_numpy(pf.k_cached().view(np.int16)).cuda().view(torch.bfloat16)
+    vpre = torch.from_numpy(pf.v_cached().view(np.int16)).cuda().view(torch.bfloat16)
+    for layer in (0, 1):
+        mux.mux_append_kv(pool, layer, pre, kpre, vpre)
+    batch = mux.Batch(indptr(pf.spec.n), L, pind, pids)
+    q = torch.from_numpy(np.stack([pf.q, pf.q]).view(np.int16)).cuda().view(torch.bfloat16)
+    kn = torch.from_numpy(np.stack([pf.k_new(), pf.k_new()]).view(np.int16)).cuda().view(torch.bfloat16)
+    vn = torch.from_numpy(np.stack([pf.v_new(), pf.v_new()]).view(np.int16)).cuda().view(torch.bfloat16)
+    o = torch.zeros((2, 128, Hq, d), dtype=torch.float32, device="cuda")
+    s = mux.make_side(batch, Hq, q, o, k_new=kn, v_new=vn, scale=0.125, num_layers=2, append=True,
+                      per_layer_inputs=True)
+    mux.mux_run_layer(part, 1, pool, s, None, None)
+    torch.cuda.synchronize()
+    os_ = oracle_build_side(pf, need + 4, 9, Hkv, d)
+    ref, _ = oracle.attention(pf.q, os_["kpool"], os_["vpool"], os_["qo_indptr"], os_["kv_len"],
+                              os_["page_indptr"], os_["page_ids"], 0.125)
+    for layer in (0, 1):
+        check_close(o[layer].cpu().numpy(), ref, what=f"layer {layer}")

@@ -1,0 +1,190 @@
+"""GPU parity: the CUDA path (through the C ABI) vs the CPU oracle on the same seeded bf16
+inputs.  Integer/byte results bit-exact; attention within DESIGN.md R8's tolerance
+(max-abs 2e-3 / rel 1e-2, BASELINE.json north_star)."""
+import math
+
+import numpy as np
+import pytest
+
+import oracle
+import synth
+from synth import SideData, SideSpec, Shapes, make_side
+from tests.helpers import check_close, gpu_build_side, oracle_build_side
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def mux():
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("no GPU")
+    import paper_2504_14489_b200 as m
+    m.lib()
+    return m
+
+
+def _run(mux, side, Hq, Hkv, d, decode, num_pages=None, seed=11, o_f32=True, num_splits=0, scale=None):
+    import torch
+    need = sum(side.spec.pages_needed())
+    num_pages = num_pages or need + 7
+    gs = gpu_build_side(mux, side, num_pages, seed, Hkv, d)
+    os_ = oracle_build_side(side, num_pages, seed, Hkv, d)
+    # integer page tables: library allocator == oracle allocator (bit-exact)
+    np.testing.assert_array_equal(gs["page_ids"], os_["page_ids"])
+    np.testing.assert_array_equal(gs["page_indptr"], os_["page_indptr"])
+    # pool image after append: byte-exact, including the untouched NaN-poisoned slots
+    torch.cuda.synchronize()
+    kimg = gs["pool"].k[0].view(torch.int16).cpu().numpy().view(np.uint16)
+    vimg = gs["pool"].v[0].view(torch.int16).cpu().numpy().view(np.uint16)
+    np.testing.assert_array_equal(kimg, os_["kpool"])
+    np.testing.assert_array_equal(vimg, os_["vpool"])
+    scale = scale if scale is not None else 1.0 / math.sqrt(d)
+    T = side.spec.total_new
+    o = torch.empty((T, Hq, d), dtype=torch.float32 if o_f32 else torch.bfloat16, device="cuda")
+    lse = torch.empty((T, Hq), dtype=torch.float32, device="cuda")
+    if decode:
+        ns = num_splits or mux.mux_decode_num_splits(side.spec.num_seqs, Hkv, max(side.spec.L), 148)
+        wsb = mux.mux_decode_workspace_bytes(side.spec.num_seqs, Hq, d, ns)
+        ws = torch.empty(max(wsb, 16), dtype=torch.uint8, device="cuda")
+        mux.mux_decode_attn(gs["pool"], 0, gs["batch"], Hq, gs["q"], o, lse, scale=scale, num_splits=ns, ws=ws)
+    else:
+        mux.mux_prefill_attn(gs["pool"], 0, gs["batch"], Hq, gs["q"], o, lse, scale=scale)
+    torch.cuda.synchronize()
+    ref, ref_lse = oracle.attention(side.q, os_["kpool"], os_["vpool"], os_["qo_indptr"], os_["kv_len"],
+                                    os_["page_indptr"], os_["page_ids"], scale)
+    return o.float().cpu().numpy(), lse.cpu().numpy(), ref, ref_lse, gs
+
+
+def _side(cfg_salt, spec, Hq, Hkv, d, decode=False, outliers=False):
+    return make_side(700 + cfg_salt, Shapes(Hq, Hkv, d, 1), spec, decode=decode, outliers=outliers)
+
+
+# ----------------------------------------------------------------------------- append (a1+a2)
+def test_append_and_page_tables_bitexact(mux):
+    side = _side(1, SideSpec([0, 5, 40], [33, 17, 1]), 8, 2, 128)
+    _run(mux, side, 8, 2, 128, decode=False)
+
+
+def test_shared_page_write_rejected(mux):
+    import torch
+    side = _side(2, SideSpec([0], [40]), 4, 1, 64)
+    gs = gpu_build_side(mux, side, 16, 3, 1, 64)
+    ids = [int(x) for x in gs["page_ids"]]
+    gs["pool"].share(ids[:2])
+    k = torch.zeros((1, 1, 64), dtype=torch.bfloat16, device="cuda")
+    b = mux.Batch([0, 1], [20], [0, 2], ids[:2])
+    with pytest.raises(mux.MuxError) as e:
+        mux.mux_append_kv(gs["pool"], 0, b, k, k)
+    assert e.value.code == 4
+
+
+# ----------------------------------------------------------------------------- decode (a4+a5)
+DECODE_CASES = [
+    # (d, Hq, Hkv, contexts)
+    (64, 4, 1, [256, 256, 256, 256]),                  # cfg1 decode shape
+    (128, 32, 8, [1, 15, 16, 17, 100, 257, 1000]),     # ragged, Llama-8B heads
+    (128, 64, 8, [33, 4096]),                          # g = 8 (70B)
+    (64, 16, 1, [129, 48]),                            # g = 16 (two N tiles)
+    (128, 8, 8, [513]),                                # MHA g = 1
+]
+
+
+@pytest.mark.parametrize("splits", [1, 3, 0])
+@pytest.mark.parametrize("case", range(len(DECODE_CASES)))
+def test_decode_parity(mux, case, splits):
+    d, Hq, Hkv, ctx = DECODE_CASES[case]
+    side = _side(10 + case, SideSpec([c - 1 for c in ctx], [1] * len(ctx)), Hq, Hkv, d, decode=True)
+    o, lse, ref, ref_lse, _ = _run(mux, side, Hq, Hkv, d, decode=True, num_splits=splits)
+    check_close(o, ref, what=f"decode case {case} splits {splits}")
+    assert np.max(np.abs(o - ref)) <= 2e-3
+    assert np.max(np.abs(lse - ref_lse)) <= 1e-3
+
+
+def test_decode_bf16_output_and_outliers(mux):
+    side = _side(20, SideSpec([700, 63], [1, 1]), 32, 8, 128, decode=True, outliers=True)
+    o, lse, ref, ref_lse, _ = _run(mux, side, 32, 8, 128, decode=True, o_f32=False)
+    check_close(o, ref, what="decode bf16 out")
+    assert np.max(np.abs(lse - ref_lse)) <= 1e-3
+
+
+# ----------------------------------------------------------------------------- prefill (a3)
+PREFILL_CASES = [
+    # (d, Hq, Hkv, r list, n list)
+    (64, 4, 1, [64], [128]),                          # cfg1 prefill
+    (128, 8, 2, [0], [300]),                          # several Q tiles + ragged tail, no prefix
+    (128, 4, 1, [37, 0, 200], [150, 1, 77]),          # r not page/tile aligned, n = 1 row
+    (128, 8, 1, [1000], [129]),                       # long prefix, g = 8
+    (64, 4, 4, [5], [260]),                           # MHA, d64
+    (128, 4, 2, [127, 129], [128, 255]),              # diagonal straddles two KV tiles
+]
+
+
+@pytest.mark.parametrize("case", range(len(PREFILL_CASES)))
+def test_prefill_parity(mux, case):
+    d, Hq, Hkv, r, n = PREFILL_CASES[case]
+    side = _side(30 + case, SideSpec(r, n), Hq, Hkv, d)
+    o, lse, ref, ref_lse, _ = _run(mux, side, Hq, Hkv, d, decode=False)
+    check_close(o, ref, what=f"prefill case {case}")
+    assert np.max(np.abs(o - ref)) <= 2e-3
+    assert np.max(np.abs(lse - ref_lse)) <= 1e-3
+
+
+def test_prefill_bf16_output_outliers(mux):
+    side = _side(40, SideSpec([90], [200]), 8, 2, 128, outliers=True)
+    o, lse, ref, ref_lse, _ = _run(mux, side, 8, 2, 128, decode=False, o_f32=False)
+    check_close(o, ref, what="prefill bf16 out")
+
+
+# ----------------------------------------------------------------------------- invariants on GPU
+def test_page_permutation_invariance_bitwise(mux):
+    side = _side(50, SideSpec([70, 3], [90, 40]), 8, 2, 128)
+    a = _run(mux, side, 8, 2, 128, decode=False, num_pages=40, seed=1)[0]
+    b = _run(mux, side, 8, 2, 128, decode=False, num_pages=64, seed=99)[0]
+    np.testing.assert_array_equal(a, b)
+    dside = _side(51, SideSpec([300, 31], [1, 1]), 8, 2, 128, decode=True)
+    a = _run(mux, dside, 8, 2, 128, decode=True, num_pages=40, seed=1, num_splits=2)[0]
+    b = _run(mux, dside, 8, 2, 128, decode=True, num_pages=64, seed=99, num_splits=2)[0]
+    np.testing.assert_array_equal(a, b)
+
+
+def test_gpu_deterministic_run_to_run(mux):
+    import torch
+    side = _side(52, SideSpec([10], [260]), 8, 2, 128)
+    o1, _, _, _, gs = _run(mux, side, 8, 2, 128, decode=False)
+    o2 = torch.empty((260, 8, 128), dtype=torch.float32, device="cuda")
+    mux.mux_prefill_attn(gs["pool"], 0, gs["batch"], 8, gs["q"], o2, None)
+    torch.cuda.synchronize()
+    np.testing.assert_array_equal(o1, o2.cpu().numpy())
+
+
+def test_prefix_reuse_equals_recompute_gpu(mux):
+    full = _side(53, SideSpec([0], [300]), 4, 1, 128)
+    o_full = _run(mux, full, 4, 1, 128, decode=False)[0]
+    r = 173
+    reuse = SideData(SideSpec([r], [300 - r]), full.q[r:], full.k_rows, full.v_rows)
+    o_r = _run(mux, reuse, 4, 1, 128, decode=False)[0]
+    check_close(o_r, o_full[r:], atol=2e-3, rtol=0, what="prefix reuse vs recompute")
+
+
+def test_decode_equals_prefill_n1_gpu(mux):
+    full = _side(54, SideSpec([0], [200]), 8, 2, 128)
+    o_full = _run(mux, full, 8, 2, 128, decode=False)[0]
+    for c in (1, 16, 17, 200):
+        dec = SideData(SideSpec([c - 1], [1]), full.q[c - 1:c], [full.k_rows[0][:c]], [full.v_rows[0][:c]])
+        o = _run(mux, dec, 8, 2, 128, decode=True)[0]
+        check_close(o[0], o_full[c - 1], atol=2e-3, rtol=0, what=f"decode c={c} vs prefill row")
+
+
+def test_empty_and_invalid_inputs_rejected(mux):
+    import torch
+    side = _side(55, SideSpec([0], [20]), 4, 1, 64)
+    gs = gpu_build_side(mux, side, 8, 3, 1, 64)
+    o = torch.empty((20, 4, 64), dtype=torch.float32, device="cuda")
+    bad = mux.Batch([0, 0, 20], [0, 20], [0, 0, 2], [int(x) for x in gs["page_ids"]])  # n_b = 0
+    with pytest.raises(mux.MuxError):
+        mux.mux_prefill_attn(gs["pool"], 0, bad, 4, gs["q"], o)
+    with pytest.raises(mux.MuxError):   # decode batch with 20 rows for 1 sequence
+        mux.mux_decode_attn(gs["pool"], 0, gs["batch"], 4, gs["q"], o)
+    with pytest.raises(mux.MuxError):   # Hq not a multiple of Hkv... (Hkv=1: use head_dim mismatch) layer
+        mux.mux_prefill_attn(gs["pool"], 3, gs["batch"], 4, gs["q"], o)
