@@ -6,17 +6,19 @@
 // exact reorganisation of the softmax.
 //
 // B200 design: HBM-bound, so the kernel is a page-streaming engine.
-//   grid (num_splits, Hkv, B), 5 warps: warp 4 = producer, warps 0-3 = consumers.
-//   Producer: one elected lane issues TMA (cp.async.bulk.tensor, SWIZZLE_128B) for the K
-//   and V blocks of one 16-token page (2 x d x 16 bf16 = 8 KiB at d=128) into a STAGES-deep
-//   mbarrier ring (96 KiB in flight per CTA, 2 CTAs/SM).  Page ids are prefetched 32 at a
-//   time with one coalesced warp load.
-//   Consumers: page i is processed by warp i%4 with the legacy tensor pipe (the group of
-//   g <= 8 q heads is the N=8 side, so FP32 ALU is left for the softmax):
+//   grid (num_splits, Hkv/HG, B); one CTA per SM; 9 warps: warp 8 = producer, 0-7 consumers.
+//   Producer: one lane issues TWO TMA ops per page (cp.async.bulk.tensor.5d, SWIZZLE_128B):
+//   the K and the V block of the page for all HG (<= 8) kv heads of the CTA's group — 32 KiB
+//   each at d=128, HG=8.  The per-SM TMA engine is op-rate bound (measured: 2 KiB boxes cap
+//   an SM at ~49 GB/s, 32 KiB ops at ~200 GB/s), so big boxes are what lets a 16-48 SM
+//   decode partition pull near-full HBM bandwidth.  ~192 KiB ring in flight per SM.
+//   Consumers: warp w owns kv head w%HG and every (8/HG)-th page; legacy tensor pipe (the
+//   group of g <= 8 q heads is the N=8 side, so FP32 ALU is left for the softmax):
 //     S^T[16 tok x 8 heads] = K_page[16 x d] . Q^T      (mma.m16n8k16, A = K via ldmatrix)
 //     online softmax per head column (warp shuffles over the 8 token lanes)
-//     P^T -> B fragments with movmatrix.trans (no smem round trip)
-//     O^T[d x 8] += V_page^T . P^T                      (A = V^T via ldmatrix.trans)
+//     P^T -> B fragments with movmatrix.trans (no smem round trip), P = P_hi + P_lo in
+//     two bf16 halves (~16-bit P)
+//     O^T[d x 8] += V_page^T . P_hi^T + V_page^T . P_lo^T (A = V^T via ldmatrix.trans)
 //   Warps merge their (m, l, O) states in smem at the end; with one split the CTA writes
 //   the normalised output, otherwise fp32 partials (o, m, l) for the combine kernel.
 #include <math.h>
@@ -26,8 +28,9 @@
 namespace mux {
 namespace {
 
-constexpr int kConsumerWarps = 4;
+constexpr int kConsumerWarps = 8;
 constexpr int kDecodeThreads = (kConsumerWarps + 1) * 32;
+constexpr int kRingBytes = 192 * 1024;   // K+V page stages in flight per CTA (1 CTA / SM)
 
 struct DecodeParams {
   const uint16_t* q;         // [B][Hq][D]
@@ -40,42 +43,46 @@ struct DecodeParams {
   const int32_t* page_indptr;
   const int32_t* page_ids;
   int num_splits, hq, hkv, g;
-  int page_row0;             // layer * num_pages (TMA dim-3 coordinate offset)
+  int page_row0;             // layer * num_pages (TMA page coordinate offset)
   int o_f32;
   float scale_log2;
 };
 
-template <int D, int STAGES>
+// Stage = one page (16 tokens) of K and V for the HG kv heads of this CTA's group, as
+// TMA lands it: [HG][d/64][16 rows][128 B] (SWIZZLE_128B), K block then V block.
+template <int D, int NT, int HG>
 struct DecodeSmem {
-  static constexpr int kBoxes = D / 64;                 // 64-dim TMA boxes per page per K or V
-  static constexpr int kPageBytes = D * kPage * 2;      // K (or V) bytes of one (page, kv head)
-  static constexpr int kStageBytes = 2 * kPageBytes;    // K + V
-  static constexpr int kQRows = 16;                     // up to g = 16 heads
-  static constexpr int kQStride = D + 8;                // padded row (bf16) -> conflict-free ldmatrix
-  static constexpr int kStagesOff = 0;
-  static constexpr int kQOff = STAGES * kStageBytes;
-  static constexpr int kBarOff = kQOff + kQRows * kQStride * 2;
-  static constexpr int kPageIdsOff = kBarOff + 2 * STAGES * 8;
-  static constexpr int kBytes = kPageIdsOff + 16;
-  // merge area (aliases the stage ring after the main loop)
-  static constexpr int kMergeO = 0;                                        // [warps][16 heads][D] f32
-  static constexpr int kMergeM = kConsumerWarps * 16 * D * 4;              // [warps][16]
+  static constexpr int kHeadBytes = D * kPage * 2;             // one (page, head) block of K (or V)
+  static constexpr int kStageBytes = 2 * HG * kHeadBytes;      // K + V of HG heads
+  static constexpr int kQStride = D + 8;                       // padded bf16 row -> conflict-free ldmatrix
+  static constexpr int kQRowsPerHead = 8 * NT;                 // g <= 8*NT
+  static constexpr int kQBytes = HG * kQRowsPerHead * kQStride * 2;
+  static constexpr int kRing = (kRingBytes < 224 * 1024 - kQBytes) ? kRingBytes : 224 * 1024 - kQBytes;
+  static constexpr int kStages = (kRing / kStageBytes) > 24 ? 24 : (kRing / kStageBytes);
+  static constexpr int kQOff = kStages * kStageBytes;
+  static constexpr int kBarOff = kQOff + kQBytes;
+  static constexpr int kBytes = kBarOff + 2 * kStages * 8;
+  // merge area (aliases the stage ring after the main loop): per warp 16 heads x D f32 + m, l
+  static constexpr int kMergeM = kConsumerWarps * 16 * D * 4;
   static constexpr int kMergeL = kMergeM + kConsumerWarps * 16 * 4;
-  static_assert(kMergeL + kConsumerWarps * 16 * 4 <= STAGES * kStageBytes, "merge area too big");
+  static_assert(kStages >= 2, "ring too small");
+  static_assert(kMergeL + kConsumerWarps * 16 * 4 <= kStages * kStageBytes, "merge area too big");
 };
 
-template <int D, int NT, int STAGES>
-__global__ void __launch_bounds__(kDecodeThreads, 2)
+template <int D, int NT, int HG>
+__global__ void __launch_bounds__(kDecodeThreads, 1)
     decode_kernel(const __grid_constant__ CUtensorMap tmap_k, const __grid_constant__ CUtensorMap tmap_v,
                   const DecodeParams p) {
-  using L = DecodeSmem<D, STAGES>;
+  using L = DecodeSmem<D, NT, HG>;
+  constexpr int STAGES = L::kStages;
+  constexpr int kWarpsPerHead = kConsumerWarps / HG;  // warps sharing one head split its pages
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + L::kBarOff);
   uint64_t* empty = full + STAGES;
   uint16_t* qs = reinterpret_cast<uint16_t*>(smem + L::kQOff);
 
-  const int split = blockIdx.x, kvh = blockIdx.y, b = blockIdx.z;
+  const int split = blockIdx.x, grp = blockIdx.y, b = blockIdx.z;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int kv_len = __ldg(p.kv_len + b);
   const int npages = (kv_len + kPage - 1) / kPage;
@@ -88,23 +95,25 @@ __global__ void __launch_bounds__(kDecodeThreads, 2)
   if (threadIdx.x == 0) {
     for (int s = 0; s < STAGES; ++s) {
       dev::mbar_init(&full[s], 1);
-      dev::mbar_init(&empty[s], 1);
+      dev::mbar_init(&empty[s], HG);   // every head's consuming warp releases the stage
     }
     dev::fence_mbar_init();
   }
-  // Q of the g heads sharing kv head `kvh` -> padded smem rows; rows >= g are zero
+  // Q rows of the HG*g q heads of this group -> [HG][8*NT][D+8] padded smem; rows >= g are zero
   {
-    const uint16_t* qsrc = p.q + (static_cast<size_t>(b) * p.hq + static_cast<size_t>(kvh) * p.g) * D;
-    for (int i = threadIdx.x; i < 8 * NT * (D / 8); i += kDecodeThreads) {
-      const int h = i / (D / 8), c = i % (D / 8);
+    const uint16_t* qsrc = p.q + (static_cast<size_t>(b) * p.hq + static_cast<size_t>(grp) * HG * p.g) * D;
+    for (int i = threadIdx.x; i < HG * L::kQRowsPerHead * (D / 8); i += kDecodeThreads) {
+      const int row = i / (D / 8), c = i % (D / 8);
+      const int hh = row / L::kQRowsPerHead, r = row % L::kQRowsPerHead;
       uint4 v = make_uint4(0, 0, 0, 0);
-      if (h < p.g) v = __ldg(reinterpret_cast<const uint4*>(qsrc + static_cast<size_t>(h) * D) + c);
-      *reinterpret_cast<uint4*>(qs + h * L::kQStride + c * 8) = v;
+      if (r < p.g) v = __ldg(reinterpret_cast<const uint4*>(qsrc + static_cast<size_t>(hh * p.g + r) * D) + c);
+      *reinterpret_cast<uint4*>(qs + row * L::kQStride + c * 8) = v;
     }
   }
   __syncthreads();
 
-  // per-thread softmax state (heads 2*(lane%4)+{0,1} of each 8-head tile), O^T accumulators
+  const int hw = warp % HG;            // kv head (within the group) of this consumer warp
+  const int pl = warp / HG;            // its page lane among the warps of that head
   float m_run[NT][2], l_run[NT][2];
   float oacc[D / 16][NT][4];
 #pragma unroll
@@ -116,7 +125,7 @@ __global__ void __launch_bounds__(kDecodeThreads, 2)
   }
 
   if (warp == kConsumerWarps) {
-    // ------------------------------------------------------------ producer
+    // ------------------------------------------------------------ producer: 2 TMA ops per page
     if (lane == 0) {
       dev::tma_prefetch(&tmap_k);
       dev::tma_prefetch(&tmap_v);
@@ -129,47 +138,42 @@ __global__ void __launch_bounds__(kDecodeThreads, 2)
       if (lane == 0) {
         if (i >= STAGES) dev::mbar_wait(&empty[s], ((i / STAGES) - 1) & 1);
         dev::mbar_expect_tx(&full[s], L::kStageBytes);
-        uint8_t* kdst = smem + L::kStagesOff + s * L::kStageBytes;
-        uint8_t* vdst = kdst + L::kPageBytes;
-#pragma unroll
-        for (int bx = 0; bx < L::kBoxes; ++bx) {
-          dev::tma_load_4d(kdst + bx * 2048, &tmap_k, &full[s], bx * 64, 0, kvh, p.page_row0 + page);
-          dev::tma_load_4d(vdst + bx * 2048, &tmap_v, &full[s], bx * 64, 0, kvh, p.page_row0 + page);
-        }
+        uint8_t* kdst = smem + s * L::kStageBytes;
+        dev::tma_load_5d(kdst, &tmap_k, &full[s], 0, 0, 0, grp * HG, p.page_row0 + page);
+        dev::tma_load_5d(kdst + HG * L::kHeadBytes, &tmap_v, &full[s], 0, 0, 0, grp * HG, p.page_row0 + page);
       }
     }
   } else {
     // ------------------------------------------------------------ consumers
-    // Q^T B-fragments: b0 = Q[head g][16kc + 2q..], b1 = Q[head g][16kc + 8 + 2q..]
     uint32_t qf[NT][D / 16][2];
 #pragma unroll
     for (int nt = 0; nt < NT; ++nt) {
 #pragma unroll
       for (int kc = 0; kc < D / 16; kc += 2) {
-        const int mi = lane >> 3;                        // matrix: (kc,lo) (kc,hi) (kc+1,lo) (kc+1,hi)
-        const int row = nt * 8 + (lane & 7);
-        const int chunk = 2 * kc + mi;                   // 8-dim chunk
+        const int mi = lane >> 3;
+        const int row = hw * L::kQRowsPerHead + nt * 8 + (lane & 7);
+        const int chunk = 2 * kc + mi;
         dev::ldsm_x4(dev::smem_u32(qs + row * L::kQStride + chunk * 8), qf[nt][kc][0], qf[nt][kc][1],
                      qf[nt][kc + 1][0], qf[nt][kc + 1][1]);
       }
     }
-    const int g4 = lane >> 2, q4 = lane & 3;
-    for (int i = warp; i < n_my; i += kConsumerWarps) {
+    const int g4 = lane >> 2;
+    for (int i = pl; i < n_my; i += kWarpsPerHead) {
       const int s = i % STAGES;
       dev::mbar_wait(&full[s], (i / STAGES) & 1);
-      uint8_t* kbuf = smem + L::kStagesOff + s * L::kStageBytes;
-      uint8_t* vbuf = kbuf + L::kPageBytes;
+      uint8_t* kbuf = smem + s * L::kStageBytes + hw * L::kHeadBytes;
+      uint8_t* vbuf = kbuf + HG * L::kHeadBytes;
       const int pos0 = (pg0 + i) * kPage;
       const int valid = min(kPage, kv_len - pos0);
       if (valid < kPage) {
-        // slots past the sequence end may hold anything (NaN-poisoned in tests): zero V rows
-        // so that P = 0 never meets NaN in the PV MMA; K rows are masked by select below.
+        // slots past the sequence end may hold anything (NaN-poisoned in tests): zero this
+        // head's V rows so P = 0 never meets NaN in the PV MMA; K rows are masked by select.
         for (int r = valid; r < kPage; ++r)
-          for (int c = lane; c < L::kBoxes * 8; c += 32)
+          for (int c = lane; c < (D / 64) * 8; c += 32)
             *reinterpret_cast<uint4*>(vbuf + (c >> 3) * 2048 + r * 128 + (c & 7) * 16) = make_uint4(0, 0, 0, 0);
         __syncwarp();
       }
-      // ---- S^T = K . Q^T
+      // ---- S^T[16 tok x 8 heads] = K . Q^T
       float sacc[NT][4];
 #pragma unroll
       for (int nt = 0; nt < NT; ++nt) sacc[nt][0] = sacc[nt][1] = sacc[nt][2] = sacc[nt][3] = 0.f;
@@ -184,9 +188,9 @@ __global__ void __launch_bounds__(kDecodeThreads, 2)
 #pragma unroll
         for (int nt = 0; nt < NT; ++nt) dev::mma_bf16_16816(sacc[nt], a0, a1, a2, a3, qf[nt][kc][0], qf[nt][kc][1]);
       }
-      // ---- online softmax (log2 domain); thread holds tokens g4, g4+8 x heads 2q4, 2q4+1
+      // ---- online softmax (log2 domain); thread holds tokens g4, g4+8 x heads 2q, 2q+1
       const bool v0 = g4 < valid, v1 = (g4 + 8) < valid;
-      uint32_t pb[NT][2];
+      uint32_t ph[NT][2], plo[NT][2];
       float alpha[NT][2];
 #pragma unroll
       for (int nt = 0; nt < NT; ++nt) {
@@ -210,10 +214,16 @@ __global__ void __launch_bounds__(kDecodeThreads, 2)
         const float p2 = dev::ex2(x[2] - mn0), p3 = dev::ex2(x[3] - mn1);
         l_run[nt][0] = l_run[nt][0] * alpha[nt][0] + p0 + p2;
         l_run[nt][1] = l_run[nt][1] * alpha[nt][1] + p1 + p3;
-        pb[nt][0] = dev::movmatrix_t(dev::pack_bf16(p0, p1));   // tokens 0-7  -> b0
-        pb[nt][1] = dev::movmatrix_t(dev::pack_bf16(p2, p3));   // tokens 8-15 -> b1
+        // P = P_hi + P_lo, both bf16: ~16 significant bits
+        const uint32_t h01 = dev::pack_bf16(p0, p1), h23 = dev::pack_bf16(p2, p3);
+        const uint32_t l01 = dev::pack_bf16(p0 - dev::bf16lo(h01), p1 - dev::bf16hi(h01));
+        const uint32_t l23 = dev::pack_bf16(p2 - dev::bf16lo(h23), p3 - dev::bf16hi(h23));
+        ph[nt][0] = dev::movmatrix_t(h01);    // tokens 0-7  -> b0
+        ph[nt][1] = dev::movmatrix_t(h23);    // tokens 8-15 -> b1
+        plo[nt][0] = dev::movmatrix_t(l01);
+        plo[nt][1] = dev::movmatrix_t(l23);
       }
-      // ---- O^T = alpha * O^T + V^T . P^T
+      // ---- O^T = alpha * O^T + V^T . (P_hi + P_lo)^T
       const uint32_t vbase = dev::smem_u32(vbuf);
 #pragma unroll
       for (int mt = 0; mt < D / 16; ++mt) {
@@ -228,13 +238,13 @@ __global__ void __launch_bounds__(kDecodeThreads, 2)
           oacc[mt][nt][1] *= alpha[nt][1];
           oacc[mt][nt][2] *= alpha[nt][0];
           oacc[mt][nt][3] *= alpha[nt][1];
-          dev::mma_bf16_16816(oacc[mt][nt], a0, a1, a2, a3, pb[nt][0], pb[nt][1]);
+          dev::mma_bf16_16816(oacc[mt][nt], a0, a1, a2, a3, ph[nt][0], ph[nt][1]);
+          dev::mma_bf16_16816(oacc[mt][nt], a0, a1, a2, a3, plo[nt][0], plo[nt][1]);
         }
       }
       __syncwarp();
       if (lane == 0) dev::mbar_arrive(&empty[s]);
     }
-    // finish row sums over the 8 token lanes
 #pragma unroll
     for (int nt = 0; nt < NT; ++nt)
 #pragma unroll
@@ -245,7 +255,7 @@ __global__ void __launch_bounds__(kDecodeThreads, 2)
   }
   __syncthreads();  // all TMA traffic consumed: the stage ring becomes the merge area
 
-  float* mo = reinterpret_cast<float*>(smem + L::kMergeO);
+  float* mo = reinterpret_cast<float*>(smem);
   float* mm = reinterpret_cast<float*>(smem + L::kMergeM);
   float* ml = reinterpret_cast<float*>(smem + L::kMergeL);
   if (warp < kConsumerWarps) {
@@ -259,9 +269,9 @@ __global__ void __launch_bounds__(kDecodeThreads, 2)
         ml[warp * 16 + h0] = l_run[nt][0];
         ml[warp * 16 + h0 + 1] = l_run[nt][1];
       }
+      float* base = mo + (warp * 16) * D;
 #pragma unroll
       for (int mt = 0; mt < D / 16; ++mt) {
-        float* base = mo + (warp * 16) * D;
         base[h0 * D + mt * 16 + g4] = oacc[mt][nt][0];
         base[(h0 + 1) * D + mt * 16 + g4] = oacc[mt][nt][1];
         base[h0 * D + mt * 16 + g4 + 8] = oacc[mt][nt][2];
@@ -270,25 +280,25 @@ __global__ void __launch_bounds__(kDecodeThreads, 2)
     }
   }
   __syncthreads();
-  // combine the 4 warp states: element (head, dim) per thread
-  const int heads = p.g;
-  for (int e = threadIdx.x; e < heads * D; e += kDecodeThreads) {
-    const int h = e / D, c = e % D;
+  // merge the warps of each head: element (head-in-group, q head, dim) per thread
+  for (int e = threadIdx.x; e < HG * p.g * D; e += kDecodeThreads) {
+    const int c = e % D, hq_in = (e / D) % p.g, hh = e / (D * p.g);
     float M = -INFINITY;
 #pragma unroll
-    for (int w = 0; w < kConsumerWarps; ++w) M = fmaxf(M, mm[w * 16 + h]);
+    for (int k = 0; k < kWarpsPerHead; ++k) M = fmaxf(M, mm[(hh + k * HG) * 16 + hq_in]);
     float Ls = 0.f, acc = 0.f;
     if (M != -INFINITY) {
 #pragma unroll
-      for (int w = 0; w < kConsumerWarps; ++w) {
-        const float mw = mm[w * 16 + h];
+      for (int k = 0; k < kWarpsPerHead; ++k) {
+        const int w = hh + k * HG;
+        const float mw = mm[w * 16 + hq_in];
         if (mw == -INFINITY) continue;
         const float sc = dev::ex2(mw - M);
-        Ls += sc * ml[w * 16 + h];
-        acc += sc * mo[(w * 16 + h) * D + c];
+        Ls += sc * ml[w * 16 + hq_in];
+        acc += sc * mo[(w * 16 + hq_in) * D + c];
       }
     }
-    const int qh = kvh * p.g + h;
+    const int qh = (grp * HG + hh) * p.g + hq_in;
     const size_t row = static_cast<size_t>(b) * p.hq + qh;
     if (p.num_splits == 1) {
       const float out = acc / Ls;
@@ -332,20 +342,18 @@ __global__ void __launch_bounds__(D) combine_kernel(const float* __restrict__ pa
   if (c == 0 && lse) lse[row] = (M + __log2f(W)) * 0.69314718055994531f;
 }
 
-constexpr int kStages = 12;
-
-template <int D, int NT>
-int launch_decode(mux_pool* pool, const DecodeParams& prm, int B, cudaStream_t st) {
-  using L = DecodeSmem<D, kStages>;
-  auto kern = decode_kernel<D, NT, kStages>;
+template <int D, int NT, int HG>
+int launch_decode_hg(mux_pool* pool, const DecodeParams& prm, int B, cudaStream_t st) {
+  using L = DecodeSmem<D, NT, HG>;
+  auto kern = decode_kernel<D, NT, HG>;
   const int smem = L::kBytes + 1024;
   static bool attr_done = false;
   if (!attr_done) {
     MUX_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
     attr_done = true;
   }
-  dim3 grid(prm.num_splits, prm.hkv, B);
-  kern<<<grid, kDecodeThreads, smem, st>>>(pool->tmap_k, pool->tmap_v, prm);
+  dim3 grid(prm.num_splits, prm.hkv / HG, B);
+  kern<<<grid, kDecodeThreads, smem, st>>>(pool->tmap_kg, pool->tmap_vg, prm);
   MUX_CUDA(cudaGetLastError());
   if (prm.num_splits > 1) {
     combine_kernel<D><<<B * prm.hq, D, 0, st>>>(prm.part_o, prm.part_m, prm.part_l, prm.o, prm.lse,
@@ -353,6 +361,17 @@ int launch_decode(mux_pool* pool, const DecodeParams& prm, int B, cudaStream_t s
     MUX_CUDA(cudaGetLastError());
   }
   return MUX_OK;
+}
+
+template <int D, int NT>
+int launch_decode(mux_pool* pool, const DecodeParams& prm, int B, cudaStream_t st) {
+  switch (pool->hg) {
+    case 8: return launch_decode_hg<D, NT, 8>(pool, prm, B, st);
+    case 4: return launch_decode_hg<D, NT, 4>(pool, prm, B, st);
+    case 2: return launch_decode_hg<D, NT, 2>(pool, prm, B, st);
+    case 1: return launch_decode_hg<D, NT, 1>(pool, prm, B, st);
+    default: return fail(MUX_ERR_UNSUPPORTED, "Hkv must be a multiple of 1, 2, 4 or 8");
+  }
 }
 
 }  // namespace
@@ -371,11 +390,14 @@ size_t mux_decode_workspace_bytes(int32_t num_seqs, int32_t hq, int32_t d, int32
 int32_t mux_decode_num_splits(int32_t num_seqs, int32_t hkv, int32_t max_kv, int32_t num_sms) {
   if (num_seqs < 1 || hkv < 1 || max_kv < 1) return 1;
   if (num_sms < 1) num_sms = 148;
-  const int64_t ctas = static_cast<int64_t>(num_seqs) * hkv;
-  const int64_t target = static_cast<int64_t>(num_sms) * 2 * 2;   // >= 2 waves of 2 CTAs/SM
+  int hg = 1;
+  for (int c = 1; c <= 8; ++c)
+    if (hkv % c == 0) hg = c;
+  const int64_t ctas = static_cast<int64_t>(num_seqs) * (hkv / hg);   // CTAs per split (1 CTA / SM)
+  const int64_t target = static_cast<int64_t>(num_sms) * 2;           // >= 2 waves
   int64_t s = (target + ctas - 1) / ctas;
   const int64_t pages = (max_kv + kPage - 1) / kPage;
-  const int64_t cap = pages / 4 > 1 ? pages / 4 : 1;                 // >= 4 pages per split
+  const int64_t cap = pages / 8 > 1 ? pages / 8 : 1;                   // >= 8 pages per split
   if (s > cap) s = cap;
   if (s > 64) s = 64;
   if (s < 1) s = 1;

@@ -23,16 +23,21 @@ static uint64_t splitmix64(uint64_t& s) {
 int pool_tmaps(mux_pool* p) {
   if (p->tmaps_ready) return MUX_OK;
   const auto& d = p->desc;
-  uint64_t dims[4] = {static_cast<uint64_t>(d.head_dim), static_cast<uint64_t>(kPage),
-                      static_cast<uint64_t>(d.num_kv_heads),
+  const uint64_t D = static_cast<uint64_t>(d.head_dim);
+  uint64_t dims[5] = {64, static_cast<uint64_t>(kPage), D / 64, static_cast<uint64_t>(d.num_kv_heads),
                       static_cast<uint64_t>(d.num_layers) * static_cast<uint64_t>(d.num_pages)};
-  uint64_t strides[3] = {static_cast<uint64_t>(d.head_dim) * 2, static_cast<uint64_t>(kPage) * d.head_dim * 2,
-                         static_cast<uint64_t>(d.num_kv_heads) * kPage * d.head_dim * 2};
-  uint32_t box[4] = {64, static_cast<uint32_t>(kPage), 1, 1};
-  int rc = make_tmap_bf16(&p->tmap_k, d.k_storage, 4, dims, strides, box);
-  if (rc) return rc;
-  rc = make_tmap_bf16(&p->tmap_v, d.v_storage, 4, dims, strides, box);
-  if (rc) return rc;
+  uint64_t strides[4] = {D * 2, 128, kPage * D * 2, static_cast<uint64_t>(d.num_kv_heads) * kPage * D * 2};
+  int hg = 1;
+  for (int c = 1; c <= 8; ++c)
+    if (d.num_kv_heads % c == 0) hg = c;
+  p->hg = hg;
+  uint32_t box1[5] = {64, static_cast<uint32_t>(kPage), static_cast<uint32_t>(D / 64), 1, 1};
+  uint32_t boxg[5] = {64, static_cast<uint32_t>(kPage), static_cast<uint32_t>(D / 64), static_cast<uint32_t>(hg), 1};
+  int rc;
+  if ((rc = make_tmap_bf16(&p->tmap_k1, d.k_storage, 5, dims, strides, box1))) return rc;
+  if ((rc = make_tmap_bf16(&p->tmap_v1, d.v_storage, 5, dims, strides, box1))) return rc;
+  if ((rc = make_tmap_bf16(&p->tmap_kg, d.k_storage, 5, dims, strides, boxg))) return rc;
+  if ((rc = make_tmap_bf16(&p->tmap_vg, d.v_storage, 5, dims, strides, boxg))) return rc;
   p->tmaps_ready = true;
   return MUX_OK;
 }

@@ -130,8 +130,8 @@ def test_n_pl_matches_paper_formula(mux):
 
 
 def test_decode_split_heuristic_and_workspace(mux):
-    assert mux.mux_decode_num_splits(64, 8, 4096, 148) == 2
-    assert mux.mux_decode_num_splits(4, 1, 256, 148) == 4          # capped at pages/4
+    assert mux.mux_decode_num_splits(64, 8, 4096, 148) == 5
+    assert mux.mux_decode_num_splits(4, 1, 256, 148) == 2          # capped at pages/8
     assert mux.mux_decode_num_splits(1, 1, 16, 148) == 1
     assert mux.mux_decode_workspace_bytes(64, 32, 128, 1) == 0
     assert mux.mux_decode_workspace_bytes(2, 4, 64, 3) >= 2 * 4 * 3 * (64 + 2) * 4
