@@ -38,6 +38,8 @@ int pool_tmaps(mux_pool* p) {
   if ((rc = make_tmap_bf16(&p->tmap_v1, d.v_storage, 5, dims, strides, box1))) return rc;
   if ((rc = make_tmap_bf16(&p->tmap_kg, d.k_storage, 5, dims, strides, boxg))) return rc;
   if ((rc = make_tmap_bf16(&p->tmap_vg, d.v_storage, 5, dims, strides, boxg))) return rc;
+  uint32_t boxh[5] = {64, static_cast<uint32_t>(kPage), 1, 1, 1};
+  if ((rc = make_tmap_bf16(&p->tmap_kh, d.k_storage, 5, dims, strides, boxh))) return rc;
   p->tmaps_ready = true;
   return MUX_OK;
 }

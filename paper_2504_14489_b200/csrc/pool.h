@@ -14,7 +14,8 @@ struct mux_pool {
   // 5-D views of K and V: {64 dims, 16 slots, d/64 halves, Hkv, layers*pages}, SWIZZLE_128B.
   // tmap_*1: box = one (page, kv head) block (both 64-dim halves, 4 KiB at d=128)   -> prefill
   // tmap_*g: box = one page of a whole kv-head group of hg heads (hg x 4 KiB)        -> decode
-  CUtensorMap tmap_k1, tmap_v1, tmap_kg, tmap_vg;
+  // tmap_kh: box = one 64-dim half of one (page, kv head) block (2 KiB)            -> prefill K
+  CUtensorMap tmap_k1, tmap_v1, tmap_kg, tmap_vg, tmap_kh;
   int hg = 1;                        // kv heads per decode CTA (largest divisor of Hkv <= 8)
   int64_t layer_elems() const {      // elements per layer of K (or V)
     return static_cast<int64_t>(desc.num_pages) * desc.num_kv_heads * mux::kPage * desc.head_dim;
