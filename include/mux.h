@@ -98,6 +98,12 @@ int mux_pool_refcount(mux_pool_t pool, int32_t page, int32_t* out);
 /* copy the current free list (front first) to out (host, capacity cap); *n_out = length */
 int mux_pool_free_list(mux_pool_t pool, int32_t* out, int32_t cap, int32_t* n_out);
 int mux_pool_storage(mux_pool_t pool, void** k_storage, void** v_storage);
+/* Sticky device-side error bits of kernels that used this pool (synchronises the device).
+ * bit 0 (MUX_POOL_ERR_V_RANGE): the prefill kernel met a V value with |v| >= 65536, outside the
+ * fp16 range its P.V product runs in; the value was clamped to
+ * +-65504 and that call's output is not within tolerance.  clear != 0 resets the bits. */
+#define MUX_POOL_ERR_V_RANGE 1u
+int mux_pool_error_flags(mux_pool_t pool, uint32_t* flags, int32_t clear);
 
 /* ------------------------------------------------------------------------------------
  * Batch descriptor shared by append / prefill / decode.

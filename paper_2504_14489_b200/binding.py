@@ -74,6 +74,7 @@ def lib():
         "mux_pool_refcount": [c_p, c_i32, ctypes.POINTER(c_i32)],
         "mux_pool_free_list": [c_p, c_p, c_i32, ctypes.POINTER(c_i32)],
         "mux_pool_storage": [c_p, ctypes.POINTER(c_p), ctypes.POINTER(c_p)],
+        "mux_pool_error_flags": [c_p, ctypes.POINTER(ctypes.c_uint32), c_i32],
         "mux_append_kv": [c_p, c_i32, ctypes.POINTER(BatchC), c_p, c_p, c_p],
         "mux_prefill_attn": [c_p, c_i32, ctypes.POINTER(BatchC), c_i32, c_p, c_p, c_i32, c_p, c_f32, c_p],
         "mux_decode_attn": [c_p, c_i32, ctypes.POINTER(BatchC), c_i32, c_p, c_p, c_i32, c_p, c_f32, c_i32, c_p,
@@ -193,6 +194,11 @@ class Pool:
         out = np.zeros(max(1, n.value), np.int32)
         _check(lib().mux_pool_free_list(self.h, out.ctypes.data, n.value, ctypes.byref(n)))
         return [int(x) for x in out[:n.value]]
+
+    def error_flags(self, clear: bool = False) -> int:
+        f = ctypes.c_uint32()
+        _check(lib().mux_pool_error_flags(self.h, ctypes.byref(f), 1 if clear else 0))
+        return f.value
 
     def page_tables(self, pages_needed: Sequence[int]):
         ind, ids = [0], []

@@ -133,6 +133,14 @@ __device__ __forceinline__ void tma_load_5d(void* dst, const CUtensorMap* map, u
       "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(c2), "r"(c3), "r"(c4), "r"(smem_u32(bar))
       : "memory");
 }
+__device__ __forceinline__ uint4 lds128(uint32_t addr) {
+  uint4 v;
+  asm volatile("ld.shared.v4.u32 {%0,%1,%2,%3}, [%4];" : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "r"(addr));
+  return v;
+}
+__device__ __forceinline__ void sts128(uint32_t addr, const uint4& v) {
+  asm volatile("st.shared.v4.u32 [%0], {%1,%2,%3,%4};" ::"r"(addr), "r"(v.x), "r"(v.y), "r"(v.z), "r"(v.w) : "memory");
+}
 __device__ __forceinline__ void fence_proxy_async_smem() {
   asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
 }
@@ -192,11 +200,37 @@ __device__ __forceinline__ uint64_t fadd2(uint64_t a, uint64_t b) {
   asm("add.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
   return d;
 }
+// 2^a, 2^b on the FMA pipe (offloads the MUFU unit): round-to-nearest split a = r + f with
+// the 1.5*2^23 trick, 2^f on [-0.5, 0.5] by a degree-4 polynomial (max rel. error 7.6e-6, well
+// below the fp16 rounding of P), exponent add of r.  Inputs are clamped to >= -125 (2^-125 is
+// zero for an fp16 P anyway).
+__device__ __forceinline__ void ex2_poly_pair(float a, float b, float& e0, float& e1) {
+  a = fmaxf(a, -125.f);
+  b = fmaxf(b, -125.f);
+  const uint64_t x = f2pack(a, b);
+  const uint64_t t = fadd2(x, f2pack(12582912.f, 12582912.f));
+  const uint64_t r = fadd2(t, f2pack(-12582912.f, -12582912.f));
+  const uint64_t f = ffma2(r, f2pack(-1.f, -1.f), x);
+  uint64_t p = ffma2(f2pack(0.009278289f, 0.009278289f), f, f2pack(0.05586502f, 0.05586502f));
+  p = ffma2(p, f, f2pack(0.24030896f, 0.24030896f));
+  p = ffma2(p, f, f2pack(0.69312954f, 0.69312954f));
+  p = ffma2(p, f, f2pack(0.99999785f, 0.99999785f));
+  float p0, p1, t0, t1;
+  f2unpack(p, p0, p1);
+  f2unpack(t, t0, t1);
+  e0 = __uint_as_float(__float_as_uint(p0) + (__float_as_uint(t0) << 23));
+  e1 = __uint_as_float(__float_as_uint(p1) + (__float_as_uint(t1) << 23));
+}
 __device__ __forceinline__ float bf16lo(uint32_t x) { return __uint_as_float(x << 16); }
 __device__ __forceinline__ float bf16hi(uint32_t x) { return __uint_as_float(x & 0xFFFF0000u); }
 __device__ __forceinline__ uint32_t pack_f16(float lo, float hi) {
   uint32_t r;
   asm("cvt.rn.f16x2.f32 %0, %1, %2;" : "=r"(r) : "f"(hi), "f"(lo));
+  return r;
+}
+__device__ __forceinline__ uint32_t pack_f16_satfinite(float lo, float hi) {
+  uint32_t r;
+  asm("cvt.rn.satfinite.f16x2.f32 %0, %1, %2;" : "=r"(r) : "f"(hi), "f"(lo));
   return r;
 }
 __device__ __forceinline__ float ex2(float x) {
@@ -301,6 +335,14 @@ __device__ __forceinline__ uint64_t umma_desc_sw128(uint32_t smem_addr, uint32_t
   d |= static_cast<uint64_t>(1) << 46;  // version = 1 (Blackwell)
   d |= static_cast<uint64_t>(2) << 61;  // SWIZZLE_128B
   return d;
+}
+// instruction descriptor, kind::f16: fp16 x fp16 -> f32
+__host__ __device__ constexpr uint32_t umma_idesc_f16(int M, int N, int a_mn_major, int b_mn_major) {
+  return (1u << 4)                                   // D format f32; A, B format 0 = f16
+         | (static_cast<uint32_t>(a_mn_major) << 15) //
+         | (static_cast<uint32_t>(b_mn_major) << 16) //
+         | (static_cast<uint32_t>(N >> 3) << 17)     //
+         | (static_cast<uint32_t>(M >> 4) << 24);
 }
 // instruction descriptor, kind::f16: bf16 x bf16 -> f32
 __host__ __device__ constexpr uint32_t umma_idesc_bf16(int M, int N, int a_mn_major, int b_mn_major) {

@@ -40,6 +40,10 @@ int pool_tmaps(mux_pool* p) {
   if ((rc = make_tmap_bf16(&p->tmap_vg, d.v_storage, 5, dims, strides, boxg))) return rc;
   uint32_t boxh[5] = {64, static_cast<uint32_t>(kPage), 1, 1, 1};
   if ((rc = make_tmap_bf16(&p->tmap_kh, d.k_storage, 5, dims, strides, boxh))) return rc;
+  if (!p->d_err) {
+    MUX_CUDA(cudaMalloc(&p->d_err, sizeof(int)));
+    MUX_CUDA(cudaMemset(p->d_err, 0, sizeof(int)));
+  }
   p->tmaps_ready = true;
   return MUX_OK;
 }
@@ -132,6 +136,7 @@ int mux_pool_create(mux_pool_t* out, const mux_pool_desc* desc) {
 
 int mux_pool_destroy(mux_pool_t p) {
   if (!p) return MUX_OK;
+  if (p->d_err) cudaFree(p->d_err);
   if (p->owns_storage) {
     cudaFree(p->desc.k_storage);
     cudaFree(p->desc.v_storage);
@@ -197,6 +202,17 @@ int mux_pool_free_list(mux_pool_t p, int32_t* out, int32_t cap, int32_t* n_out) 
     ++n;
   }
   *n_out = n;
+  return MUX_OK;
+}
+
+int mux_pool_error_flags(mux_pool_t p, uint32_t* flags, int32_t clear) {
+  if (!p || !flags) return fail(MUX_ERR_INVALID_ARG, "bad argument");
+  *flags = 0;
+  if (!p->d_err) return MUX_OK;
+  int v = 0;
+  MUX_CUDA(cudaMemcpy(&v, p->d_err, sizeof(int), cudaMemcpyDeviceToHost));
+  *flags = static_cast<uint32_t>(v);
+  if (clear) MUX_CUDA(cudaMemset(p->d_err, 0, sizeof(int)));
   return MUX_OK;
 }
 

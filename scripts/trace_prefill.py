@@ -22,7 +22,7 @@ del os.environ["MUX_PF_TRACE"]
 t = tr.view(16, 256).cpu().numpy().astype(np.int64)
 nt = (N + 127) // 128
 t0 = t[t > 0].min()
-names = ["sfull0", "sfull1", "pass1_0", "pass1_1", "pfull0", "pfull1", "pv0", "pv1", "qk0", "qk1", "kload", "vload", "exp0", "exp1", "stw0", "stw1"]
+names = ["sfull0", "sfull1", "pass1_0", "pass1_1", "pfull0", "pfull1", "pv0", "pv1", "qk0", "qk1", "kload", "vload", "exp0", "exp1", "conv", "-"]
 print("j " + " ".join(f"{n:>8s}" for n in names))
 for j in list(range(0, 6)) + list(range(nt - 4, nt)):
     print(f"{j:2d} " + " ".join(f"{(t[e, j] - t0) if t[e, j] else -1:8d}" for e in range(16)))
@@ -30,4 +30,4 @@ sf = t[0, 1:nt] - t[0, :nt - 1]
 print("period sfull0 median", np.median(sf[5:]), "softmax0 (sfull->pfull) median", np.median((t[4] - t[0])[5:nt]),
       "pass1 median", np.median((t[2] - t[0])[5:nt]), "pfull0->pv0", np.median((t[6] - t[4])[5:nt]),
       "pv0->sfull0(next)", np.median((t[0, 6:nt] - t[6, 5:nt - 1])),
-      "pass1->exp", np.median((t[12] - t[2])[5:nt]), "exp->stw", np.median((t[14] - t[12])[5:nt]), "stw->pfull", np.median((t[4] - t[14])[5:nt]))
+      "pass1->exp", np.median((t[12] - t[2])[5:nt]), "exp->pfull", np.median((t[4] - t[12])[5:nt]), "vload->conv", np.median((t[14] - t[11])[5:nt]), "conv->pfull0", np.median((t[4] - t[14])[5:nt]))

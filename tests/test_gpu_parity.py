@@ -186,3 +186,22 @@ def test_empty_and_invalid_inputs_rejected(mux):
         mux.mux_decode_attn(gs["pool"], 0, gs["batch"], 4, gs["q"], o)
     with pytest.raises(mux.MuxError):   # Hq not a multiple of Hkv... (Hkv=1: use head_dim mismatch) layer
         mux.mux_prefill_attn(gs["pool"], 3, gs["batch"], 4, gs["q"], o)
+
+
+def test_prefill_v_range_flag(mux):
+    """The prefill P.V product runs in fp16: normal data leaves the
+    pool's error word clear; a |V| >= 65536 sets MUX_POOL_ERR_V_RANGE instead of failing silently."""
+    import torch
+    side = _side(60, SideSpec([10], [100]), 4, 2, 128)
+    o, _, ref, _, gs = _run(mux, side, 4, 2, 128, decode=False)
+    check_close(o, ref, what="prefill before range test")
+    assert gs["pool"].error_flags() == 0
+    v = side.v_rows[0].copy()
+    v[50, 1, 7] = synth.f32_to_bf16_bits(np.array([1.0e6], np.float32))[0]
+    big = SideData(side.spec, side.q, side.k_rows, [v])
+    gs2 = gpu_build_side(mux, big, 16, 11, 2, 128)
+    o2 = torch.empty((100, 4, 128), dtype=torch.float32, device="cuda")
+    mux.mux_prefill_attn(gs2["pool"], 0, gs2["batch"], 4, gs2["q"], o2, None)
+    torch.cuda.synchronize()
+    assert gs2["pool"].error_flags(clear=True) & 1
+    assert gs2["pool"].error_flags() == 0
