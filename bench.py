@@ -406,15 +406,22 @@ def main():
     pf_tflops = wl.prefill_flops_layer() / pf_launch_s / 1e12
     dc_gbs = wl.decode_bytes_layer() / dc_launch_s / 1e9
     tc_peak = peaks.get("bf16_tflops_sustained", peaks["bf16_tflops"])
+    traffic = {}
+    try:
+        with open(os.path.join(ROOT, "profiles", "r01_traffic.json")) as f:
+            traffic = json.load(f)
+    except Exception:
+        pass
     pf_share = best["pf_sms"] / total_sms
     dc_share = best["dec_sms"] / total_sms
     roofline = {"bound": "tensor", "kernel": "prefill_kernel (tcgen05)", "achieved": pf_tflops,
                 "peak": tc_peak, "unit": "TFLOP/s", "frac": pf_tflops / tc_peak,
                 "frac_of_sm_share": pf_tflops / (tc_peak * pf_share), "peak_src": f"{peaks_src} bf16_tflops_sustained",
-                "traffic": None, "per_launch": "1 layer of the 8192-token causal prefill, all q heads"}
+                "traffic": traffic.get("prefill_kernel", {}).get("bytes"),
+                "per_launch": "1 layer of the 8192-token causal prefill, all q heads"}
     roofline_dec = {"bound": "hbm", "kernel": "decode_kernel", "achieved": dc_gbs, "peak": peaks["hbm_gbs"],
                     "unit": "GB/s", "frac": dc_gbs / peaks["hbm_gbs"], "peak_src": f"{peaks_src} hbm_gbs",
-                    "sm_share": dc_share, "traffic": None}
+                    "sm_share": dc_share, "traffic": traffic.get("decode_kernel", {}).get("bytes")}
     launches_per_step = wl.layers * 2 + wl.layers * iters * (2 + (1 if ns > 1 else 0)) + 4
     clocks = clk.summary()
     line = {
