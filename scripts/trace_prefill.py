@@ -20,9 +20,9 @@ mux.mux_prefill_attn(pool, 0, b, Hq, q, o)
 torch.cuda.synchronize()
 del os.environ["MUX_PF_TRACE"]
 t = tr.view(16, 256).cpu().numpy().astype(np.int64)
-nt = (N + 127) // 128
+nt = (N + 63) // 64  # sub-tiles (v5: 64-key S sub-tiles)
 t0 = t[t > 0].min()
-names = ["sfull0", "sfull1", "pass1_0", "pass1_1", "pfull0", "pfull1", "pv0", "pv1", "qk0", "qk1", "kload", "vload", "exp0", "exp1", "conv", "-"]
+names = ["sfull0", "sfull1", "pass1_0", "pass1_1", "pfull0", "pfull1", "pv0", "pv1", "qk0", "qk1", "kload", "vload", "exp0", "exp1", "qkret0", "swait0"]
 print("j " + " ".join(f"{n:>8s}" for n in names))
 for j in list(range(0, 6)) + list(range(nt - 4, nt)):
     print(f"{j:2d} " + " ".join(f"{(t[e, j] - t0) if t[e, j] else -1:8d}" for e in range(16)))
