@@ -116,6 +116,27 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
   while (!mbar_try_wait(a, parity)) {
   }
 }
+// try_wait with a suspend-time hint: the thread sleeps (instead of re-issuing the probe)
+// until the phase completes or ~hint_ns elapse, leaving issue slots to busy warps
+__device__ __forceinline__ bool mbar_try_wait_sleep(uint32_t bar, uint32_t parity, uint32_t hint_ns) {
+  uint32_t ok;
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2, %3;\n\t"
+      "selp.u32 %0, 1, 0, p;\n\t}"
+      : "=r"(ok)
+      : "r"(bar), "r"(parity), "r"(hint_ns)
+      : "memory");
+  return ok != 0;
+}
+__device__ __forceinline__ void mbar_wait_sleep(uint64_t* bar, uint32_t parity, uint32_t hint_ns = 100000) {
+  const uint32_t a = smem_u32(bar);
+  while (!mbar_try_wait_sleep(a, parity, hint_ns)) {
+  }
+}
+// warp index the compiler treats as warp-uniform (keeps TMEM / descriptor operands in
+// uniform registers, avoiding ELECT/R2UR waterfall loops)
+__device__ __forceinline__ int warp_idx_uniform() { return __shfl_sync(0xffffffffu, threadIdx.x >> 5, 0); }
 
 // ---------------------------------------------------------------- TMA
 __device__ __forceinline__ void tma_prefetch(const CUtensorMap* map) {

@@ -21,6 +21,9 @@ __global__ void k(uint32_t* out, long long* cyc, int iters) {
       if (OP == 7) asm volatile("max.f32 %0, %0, %0;" : "+r"(r[i]));
       if (OP == 8) asm volatile("mad.lo.u32 %0, %0, 8388608, %0;" : "+r"(r[i]));
       if (OP == 9) asm volatile("add.rn.f32 %0, %0, %0;" : "+r"(r[i]));
+      if (OP == 10) asm volatile("ex2.approx.f16x2 %0, %0;" : "+r"(r[i]));
+      if (OP == 11) asm volatile("ex2.approx.ftz.bf16x2 %0, %0;" : "+r"(r[i]));
+      if (OP == 12) { asm volatile("{.reg .f16 lo, hi; .reg .f32 a, b; mov.b32 {lo, hi}, %0; cvt.f32.f16 a, lo; cvt.f32.f16 b, hi; add.f32 a, a, b; mov.b32 %0, a;}" : "+r"(r[i])); }
     }
   }
   long long t1 = clock64();
@@ -43,6 +46,7 @@ int main() {
   uint32_t* out; long long* cyc; cudaMalloc(&out, 148 * 512 * 4); cudaMalloc(&cyc, 148 * 8);
   run<0>("FFMA", out, cyc); run<1>("FFMA2", out, cyc); run<2>("FADD2", out, cyc); run<3>("MUFU.EX2", out, cyc);
   run<4>("F2FP.F16", out, cyc); run<5>("PRMT", out, cyc); run<6>("LOP3", out, cyc); run<7>("FMNMX", out, cyc);
-  run<8>("IMAD", out, cyc); run<9>("FADD", out, cyc);
+  run<8>("IMAD", out, cyc); run<9>("FADD", out, cyc); run<10>("EX2.F16x2", out, cyc); run<11>("EX2.BF16x2", out, cyc);
+  run<12>("HCVT2+FADD", out, cyc);
   return 0;
 }
