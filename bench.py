@@ -7,9 +7,11 @@ the 8 configs of the 16-SM rule).
 
 A STEP is one multiplexed window through the whole hot path (all §8(a) rows):
   decode side : `iters` decode iterations x 32 layers, each layer = mux_append_kv (the
-                current token) + split-KV decode attention (+ combine);
+                current token) + split-KV decode attention (+ combine) + out-projection
+                partial GEMM (+ NCCL all-reduce of it on the decode communicator when N > 1);
   prefill side: the 8k prefill through all 32 layers, layer by layer, each layer =
-                mux_append_kv (8192 new K/V rows) + tcgen05 prefill attention,
+                mux_append_kv (8192 new K/V rows) + tcgen05 prefill attention + out-projection
+                (+ all-reduce on the prefill communicator when N > 1),
 both enqueued by ONE mux_run_layer call (decode first) on the chosen SM split.
 `iters` balances the two sides with the paper's N_PL rule evaluated on the
 isolated timings of that split, so neither side idles (bubble-less).
@@ -20,9 +22,10 @@ the step's inputs (new-token Q/K/V, one layer's worth, reused by every layer: th
 projections are outside this hot path) copied from pinned host memory and the last
 layer's outputs copied back inside the timed region.
 
-Multi-GPU (torchrun, N>1): KV-head sharding (§8(e)) — each rank holds Hkv/N kv heads and
-Hq/N q heads of the same workload (strong scaling); attention needs no collective.  The
-out-projection all-reduce row (a7) is not in the timed step yet.
+Multi-GPU (torchrun, N>1): KV-head sharding (§8(e)) — each rank holds Hkv/N kv heads,
+Hq/N q heads and the matching rows of W_o of the same workload (strong scaling); attention
+needs no collective; each layer's out-projection partial sums are all-reduced (bf16, NCCL)
+on the side's own green-context stream through a per-side communicator.
 """
 from __future__ import annotations
 
@@ -143,6 +146,13 @@ class Workload:
         self.dc_q, self.dc_k, self.dc_v = rnd(Bd, self.Hq, self.d), rnd(Bd, self.Hkv, self.d), rnd(Bd, self.Hkv, self.d)
         self.pf_o = torch.empty((Tp, self.Hq, self.d), dtype=torch.bfloat16, device=dev)
         self.dc_o = torch.empty((Bd, self.Hq, self.d), dtype=torch.bfloat16, device=dev)
+        # a7: this rank's rows of W_o (N(0, 1/(Hq d)), one matrix reused by every layer) and outputs
+        self.hidden = S.hidden
+        self.w_o = (torch.randn((self.Hq * self.d, self.hidden), generator=g, device=dev) /
+                    math.sqrt(S.Hq * self.d)).to(torch.bfloat16)
+        self.pf_y = torch.empty((Tp, self.hidden), dtype=torch.bfloat16, device=dev)
+        self.dc_y = torch.empty((Bd, self.hidden), dtype=torch.bfloat16, device=dev)
+        self.hooks = {}
         self.scale = 1.0 / math.sqrt(self.d)
         self.ws = None
 
@@ -154,11 +164,15 @@ class Workload:
         if self.ws is None or self.ws.numel() < wsb:
             self.ws = torch.empty(max(16, wsb), dtype=torch.uint8, device="cuda")
         pf = mux.make_side(self.pf_batch, self.Hq, self.pf_q, self.pf_o, k_new=self.pf_k, v_new=self.pf_v,
-                           scale=self.scale, layer0=0, num_layers=self.layers, append=True)
+                           scale=self.scale, layer0=0, num_layers=self.layers, append=True,
+                           w_o=self.w_o, y=self.pf_y, hook=self.hooks.get(1))
         dc = mux.make_side(self.dc_batch, self.Hq, self.dc_q, self.dc_o, k_new=self.dc_k, v_new=self.dc_v,
                            scale=self.scale, layer0=0, num_layers=self.layers * iters, append=True,
-                           num_splits=ns, ws=self.ws)
+                           num_splits=ns, ws=self.ws, w_o=self.w_o, y=self.dc_y, hook=self.hooks.get(0))
         return pf, dc, ns
+
+    def outproj_flops_layer(self, side):
+        return 2.0 * side.total_new * self.Hq * self.d * self.hidden
 
     # algorithmic work per layer
     def prefill_flops_layer(self):
@@ -287,6 +301,14 @@ def main():
     peaks, peaks_src = load_peaks()
 
     wl = Workload(args.config, rank, world, layers=args.layers or None)
+    comms = []
+    if world > 1:
+        # one NCCL communicator per side; each layer's out-proj partial sums are all-reduced on
+        # the side's own (green-context) stream from the mux_run_layer hook
+        from paper_2504_14489_b200 import nccl
+        comms = [nccl.Comm(rank, world), nccl.Comm(rank, world)]
+        wl.hooks = {0: lambda side, layer, stream: comms[0].all_reduce_(wl.dc_y, stream),
+                    1: lambda side, layer, stream: comms[1].all_reduce_(wl.pf_y, stream)}
     if world > 1:  # identical page tables on every rank (integer-exact check)
         h = torch.tensor([wl.page_hash], device="cuda")
         hs = [torch.zeros_like(h) for _ in range(world)]
@@ -372,8 +394,8 @@ def main():
 
     # ---- e2e through the public API: H2D of the step's inputs + D2H of the last outputs
     pin = {k: getattr(wl, k).cpu().pin_memory() for k in ("pf_q", "pf_k", "pf_v", "dc_q", "dc_k", "dc_v")}
-    out_pf = torch.empty(wl.pf_o.shape, dtype=wl.pf_o.dtype).pin_memory()
-    out_dc = torch.empty(wl.dc_o.shape, dtype=wl.dc_o.dtype).pin_memory()
+    out_pf = torch.empty(wl.pf_y.shape, dtype=wl.pf_y.dtype).pin_memory()
+    out_dc = torch.empty(wl.dc_y.shape, dtype=wl.dc_y.dtype).pin_memory()
     h2d = sum(t.numel() * t.element_size() for t in pin.values())
     d2h = out_pf.numel() * out_pf.element_size() + out_dc.numel() * out_dc.element_size()
 
@@ -381,8 +403,8 @@ def main():
         for k, t in pin.items():
             getattr(wl, k).copy_(t, non_blocking=True)
         mux.mux_run_layer(part, i, wl.pool, pf, dc, times)
-        out_pf.copy_(wl.pf_o, non_blocking=True)
-        out_dc.copy_(wl.dc_o, non_blocking=True)
+        out_pf.copy_(wl.pf_y, non_blocking=True)
+        out_dc.copy_(wl.dc_y, non_blocking=True)
     for _ in range(2):
         e2e_step()
     torch.cuda.synchronize()
@@ -401,9 +423,11 @@ def main():
     # ---- rooflines (achieved = algorithmic work per launch / average launch duration)
     pf_side_s = (tt[3] - tt[2]) * 1e-9
     dc_side_s = (tt[1] - tt[0]) * 1e-9
+    # a side's per-layer window holds append + attention + out-proj (+ all-reduce): the prefill
+    # roofline counts both tcgen05 kernels' FLOPs over the whole window (a lower bound for each)
     pf_launch_s = pf_side_s / wl.layers
     dc_launch_s = dc_side_s / (wl.layers * iters)
-    pf_tflops = wl.prefill_flops_layer() / pf_launch_s / 1e12
+    pf_tflops = (wl.prefill_flops_layer() + wl.outproj_flops_layer(wl.pf_spec)) / pf_launch_s / 1e12
     dc_gbs = wl.decode_bytes_layer() / dc_launch_s / 1e9
     tc_peak = peaks.get("bf16_tflops_sustained", peaks["bf16_tflops"])
     traffic = {}
@@ -414,15 +438,17 @@ def main():
         pass
     pf_share = best["pf_sms"] / total_sms
     dc_share = best["dec_sms"] / total_sms
-    roofline = {"bound": "tensor", "kernel": "prefill_kernel (tcgen05)", "achieved": pf_tflops,
+    roofline = {"bound": "tensor", "kernel": "prefill side per layer: prefill_kernel + outproj_kernel (tcgen05)",
+                "achieved": pf_tflops,
                 "peak": tc_peak, "unit": "TFLOP/s", "frac": pf_tflops / tc_peak,
                 "frac_of_sm_share": pf_tflops / (tc_peak * pf_share), "peak_src": f"{peaks_src} bf16_tflops_sustained",
                 "traffic": traffic.get("prefill_kernel", {}).get("bytes"),
-                "per_launch": "1 layer of the 8192-token causal prefill, all q heads"}
+                "per_launch": (f"1 layer: causal prefill attention {wl.prefill_flops_layer():.3e} FLOP + o_proj "
+                               f"{wl.pf_spec.total_new}x{wl.Hq * wl.d}x{wl.hidden} {wl.outproj_flops_layer(wl.pf_spec):.3e}")}
     roofline_dec = {"bound": "hbm", "kernel": "decode_kernel", "achieved": dc_gbs, "peak": peaks["hbm_gbs"],
                     "unit": "GB/s", "frac": dc_gbs / peaks["hbm_gbs"], "peak_src": f"{peaks_src} hbm_gbs",
                     "sm_share": dc_share, "traffic": traffic.get("decode_kernel", {}).get("bytes")}
-    launches_per_step = wl.layers * 2 + wl.layers * iters * (2 + (1 if ns > 1 else 0)) + 4
+    launches_per_step = wl.layers * 3 + wl.layers * iters * (3 + (1 if ns > 1 else 0)) + 4
     clocks = clk.summary()
     line = {
         "metric": METRIC, "value": value, "unit": "tok/s", "n_gpus": world, "steps": args.steps,
@@ -450,6 +476,8 @@ def main():
     if rank == 0:
         print(json.dumps(line), flush=True)
     part.close()
+    for c in comms:
+        c.close()
     if world > 1:
         dist.destroy_process_group()
 

@@ -187,6 +187,13 @@ int32_t mux_partition_count(mux_part_t part);
 int mux_partition_memory(mux_part_t part, int64_t* bytes);
 int32_t mux_device_sm_count(int32_t device);
 
+/* Per-layer host hook of a mux_run_layer side, called while the side's work is ENQUEUED
+ * (host side, in layer order, after that layer's attention (+ out-projection) was enqueued on
+ * `stream`).  Multi-GPU callers enqueue the layer's all-reduce of the out-projection partial
+ * sums here on the side's own communicator, so the collective runs on the side's SMs
+ * (SURVEY §8e).  side: 0 = decode, 1 = prefill. */
+typedef void (*mux_layer_hook)(void* user, int32_t side, int32_t layer_index, mux_stream_t stream);
+
 /* One side of a mux_run_layer call.  For layer i in [0, num_layers) the side processes
  * pool layer (layer0 + i) % pool_layers with inputs at base + i*stride (bytes; stride 0
  * = the same buffer every layer). */
@@ -206,6 +213,15 @@ typedef struct {
   int32_t num_splits;      /* decode only; 0 = auto for the decode partition's SM count */
   void* ws;                /* decode only */
   size_t ws_bytes;
+  /* a7 (optional, w_o == NULL: off): after each layer's attention, y = o . w_o with
+   * o [total_q][Hq*d] bf16 (o_dtype must be bf16), w_o [Hq*d][hidden] bf16, y [total_q][hidden] */
+  const void* w_o;
+  void* y;
+  int64_t w_stride, y_stride;
+  int32_t hidden;
+  int32_t y_dtype;
+  mux_layer_hook hook;     /* optional */
+  void* hook_user;
 } mux_side;
 
 /* device timestamps (%globaltimer, ns) written by 1-thread stamp kernels on each side */

@@ -41,12 +41,17 @@ class BatchC(ctypes.Structure):
                 ("h_qo_indptr", c_p), ("h_kv_len", c_p), ("h_page_indptr", c_p), ("h_page_ids", c_p)]
 
 
+LayerHook = ctypes.CFUNCTYPE(None, c_p, c_i32, c_i32, c_p)
+
+
 class SideC(ctypes.Structure):
     _fields_ = [("batch", ctypes.POINTER(BatchC)), ("num_q_heads", c_i32), ("q", c_p), ("k_new", c_p),
                 ("v_new", c_p), ("o", c_p), ("lse", c_p), ("q_stride", c_i64), ("kv_stride", c_i64),
                 ("o_stride", c_i64), ("lse_stride", c_i64), ("o_dtype", c_i32), ("scale", c_f32),
                 ("layer0", c_i32), ("num_layers", c_i32), ("append", c_i32), ("num_splits", c_i32),
-                ("ws", c_p), ("ws_bytes", c_sz)]
+                ("ws", c_p), ("ws_bytes", c_sz), ("w_o", c_p), ("y", c_p), ("w_stride", c_i64),
+                ("y_stride", c_i64), ("hidden", c_i32), ("y_dtype", c_i32), ("hook", LayerHook),
+                ("hook_user", c_p)]
 
 
 class SideTimes(ctypes.Structure):
@@ -286,6 +291,16 @@ def mux_num_prefill_layers(t_decode: float, t_prefill: float, n_layers_model: in
     return int(lib().mux_num_prefill_layers(t_decode, t_prefill, n_layers_model, remaining))
 
 
+def mux_outproj(x, w, y, stream=None):
+    """a7 partial GEMM: y[T][N] = x[T][K] . w[K][N] (bf16 in, fp32 accumulate, y bf16 or fp32)."""
+    import torch
+    T, K = x.shape
+    K2, N = w.shape
+    assert K == K2 and tuple(y.shape) == (T, N)
+    yd = MUX_DTYPE_F32 if y.dtype == torch.float32 else MUX_DTYPE_BF16
+    _check(lib().mux_outproj(_ptr(x), _ptr(w), _ptr(y), yd, T, K, N, _stream(stream)))
+
+
 def mux_device_sm_count(device: int = 0) -> int:
     return int(lib().mux_device_sm_count(device))
 
@@ -328,7 +343,7 @@ def mux_partition_create(device: int, decode_sms: Sequence[int]) -> Partition:
 
 def make_side(batch: Batch, num_q_heads: int, q, o, k_new=None, v_new=None, lse=None, scale: float = 1.0,
               layer0: int = 0, num_layers: int = 1, append: bool = False, num_splits: int = 0, ws=None,
-              per_layer_inputs: bool = False) -> SideC:
+              per_layer_inputs: bool = False, w_o=None, y=None, hook=None) -> SideC:
     """Build a mux_side.  per_layer_inputs: q/k_new/v_new/o/lse carry a leading layer dim
     and layer i uses slice i (stride = one slice); otherwise every layer reuses the buffers."""
     import torch
@@ -350,7 +365,18 @@ def make_side(batch: Batch, num_q_heads: int, q, o, k_new=None, v_new=None, lse=
     s.num_splits = num_splits
     s.ws = _ptr(ws)
     s.ws_bytes = ws.numel() * ws.element_size() if ws is not None else 0
-    s._keep = (batch, q, o, k_new, v_new, lse, ws)
+    if w_o is not None:
+        s.w_o, s.y = _ptr(w_o), _ptr(y)
+        s.w_stride = w_o[0].numel() * w_o.element_size() if w_o.dim() == 3 else 0
+        s.y_stride = y[0].numel() * y.element_size() if y.dim() == 3 else 0
+        s.hidden = int(w_o.shape[-1])
+        s.y_dtype = MUX_DTYPE_F32 if y.dtype == torch.float32 else MUX_DTYPE_BF16
+    cb = None
+    if hook is not None:
+        # hook(side, layer_index, stream_handle) -> None; enqueue work on that stream
+        cb = LayerHook(lambda user, side, layer, stream: hook(int(side), int(layer), int(stream or 0)))
+        s.hook = cb
+    s._keep = (batch, q, o, k_new, v_new, lse, ws, w_o, y, cb)
     return s
 
 

@@ -162,6 +162,8 @@ int mux_partition_memory(mux_part_t p, int64_t* bytes) {
 
 static int run_side(mux_pool_t pool, const mux_side* s, bool decode, int sms, cudaStream_t st,
                     unsigned long long* t0, unsigned long long* t1) {
+  if (s->w_o && (s->o_dtype != MUX_DTYPE_BF16 || !s->y || s->hidden < 1))
+    return fail(MUX_ERR_INVALID_ARG, "out-projection needs bf16 o, y and hidden >= 1");
   if (t0) stamp_kernel<<<1, 1, 0, st>>>(t0);
   const int nl = pool->desc.num_layers;
   int splits = 1;
@@ -190,6 +192,13 @@ static int run_side(mux_pool_t pool, const mux_side* s, bool decode, int sms, cu
       rc = mux_prefill_attn(pool, layer, s->batch, s->num_q_heads, at(s->q, s->q_stride), o, s->o_dtype, lse,
                             s->scale, reinterpret_cast<mux_stream_t>(st));
     if (rc) return rc;
+    if (s->w_o) {
+      rc = mux_outproj(o, at(s->w_o, s->w_stride), const_cast<void*>(at(s->y, s->y_stride)), s->y_dtype,
+                       s->batch->total_q, s->num_q_heads * pool->desc.head_dim, s->hidden,
+                       reinterpret_cast<mux_stream_t>(st));
+      if (rc) return rc;
+    }
+    if (s->hook) s->hook(s->hook_user, decode ? 0 : 1, i, reinterpret_cast<mux_stream_t>(st));
   }
   if (t1) stamp_kernel<<<1, 1, 0, st>>>(t1);
   MUX_CUDA(cudaGetLastError());
@@ -227,12 +236,6 @@ int mux_run_layer(mux_part_t part, int32_t split_idx, mux_pool_t pool, const mux
   if (decode) MUX_CUDA(cudaStreamWaitEvent(js, part->ev_dec, 0));
   if (prefill) MUX_CUDA(cudaStreamWaitEvent(js, part->ev_pf, 0));
   return MUX_OK;
-}
-
-int mux_outproj(const void* x, const void* w, void* y, int32_t y_dtype, int32_t T, int32_t K, int32_t N,
-                mux_stream_t stream) {
-  (void)x; (void)w; (void)y; (void)y_dtype; (void)T; (void)K; (void)N; (void)stream;
-  return fail(MUX_ERR_UNSUPPORTED, "mux_outproj: not built yet");
 }
 
 }  // extern "C"

@@ -1,0 +1,82 @@
+"""Minimal NCCL binding (ctypes over the NCCL shipped with torch) for the multi-GPU step.
+
+torch's ProcessGroupNCCL enqueues collectives on its own internal streams; the multiplexed
+engine needs each side's all-reduce of the out-projection partial sums on
+that side's green-context stream, so that the NCCL kernels run on the side's own SM
+partition and stay ordered after its layer's GEMM.  One communicator per side (two
+concurrent collectives on one communicator from two streams could serialise or deadlock).
+torch.distributed (any backend) is used only to broadcast the ncclUniqueId.
+"""
+from __future__ import annotations
+
+import ctypes
+import glob
+import os
+
+_lib = None
+
+NCCL_BF16, NCCL_F32 = 9, 7
+NCCL_SUM = 0
+
+
+class _UniqueId(ctypes.Structure):
+    _fields_ = [("internal", ctypes.c_char * 128)]
+
+
+def lib():
+    global _lib
+    if _lib is None:
+        import nvidia
+        cands = []
+        for p in nvidia.__path__:
+            cands += glob.glob(os.path.join(p, "nccl", "lib", "libnccl.so*"))
+        cands += ["libnccl.so.2"]
+        last = None
+        for c in cands:
+            try:
+                _lib = ctypes.CDLL(c)
+                break
+            except OSError as e:  # pragma: no cover
+                last = e
+        if _lib is None:
+            raise ImportError(f"NCCL not found: {last}")
+        _lib.ncclGetUniqueId.argtypes = [ctypes.POINTER(_UniqueId)]
+        _lib.ncclCommInitRank.argtypes = [ctypes.POINTER(ctypes.c_void_p), ctypes.c_int, _UniqueId, ctypes.c_int]
+        _lib.ncclAllReduce.argtypes = [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_size_t, ctypes.c_int, ctypes.c_int,
+                                       ctypes.c_void_p, ctypes.c_void_p]
+        _lib.ncclCommDestroy.argtypes = [ctypes.c_void_p]
+        _lib.ncclGetErrorString.restype = ctypes.c_char_p
+    return _lib
+
+
+def _check(rc: int, what: str):
+    if rc != 0:
+        raise RuntimeError(f"{what}: NCCL error {rc}: {lib().ncclGetErrorString(rc).decode()}")
+
+
+class Comm:
+    """A NCCL communicator over all ranks of the default torch.distributed group."""
+
+    def __init__(self, rank: int, world: int):
+        import torch.distributed as dist
+        uid = _UniqueId()
+        if rank == 0:
+            _check(lib().ncclGetUniqueId(ctypes.byref(uid)), "ncclGetUniqueId")
+        if world > 1:
+            obj = [bytes(uid.internal) if rank == 0 else None]
+            dist.broadcast_object_list(obj, src=0)
+            ctypes.memmove(ctypes.addressof(uid), obj[0], 128)
+        self.comm = ctypes.c_void_p()
+        _check(lib().ncclCommInitRank(ctypes.byref(self.comm), world, uid, rank), "ncclCommInitRank")
+
+    def all_reduce_(self, t, stream: int):
+        """In-place sum all-reduce of tensor t, enqueued on the raw CUDA stream handle `stream`."""
+        import torch
+        dt = {torch.bfloat16: NCCL_BF16, torch.float32: NCCL_F32}[t.dtype]
+        _check(lib().ncclAllReduce(t.data_ptr(), t.data_ptr(), t.numel(), dt, NCCL_SUM, self.comm, stream),
+               "ncclAllReduce")
+
+    def close(self):
+        if self.comm:
+            lib().ncclCommDestroy(self.comm)
+            self.comm = ctypes.c_void_p()

@@ -76,3 +76,20 @@ def main():
 
 if __name__ == "__main__":
     main()
+
+
+def outproj_perf():
+    for T, K, N in ((8192, 4096, 4096), (64, 4096, 4096), (8192, 1024, 8192)):
+        x = torch.randn((T, K), device="cuda").to(torch.bfloat16)
+        w = (torch.randn((K, N), device="cuda") / 64).to(torch.bfloat16)
+        y = torch.empty((T, N), device="cuda", dtype=torch.bfloat16)
+        t = timed(lambda: mux.mux_outproj(x, w, y), iters=10)
+        ref = (x.float() @ w.float())
+        err = (y.float() - ref).abs().max().item()
+        tb = timed(lambda: torch.matmul(x, w), iters=10)
+        print(f"outproj T={T} K={K} N={N}: {t*1e6:.1f} us {2*T*K*N/t/1e12:.1f} TFLOP/s (cuBLAS {2*T*K*N/tb/1e12:.1f}) max|d| {err:.3g}",
+              flush=True)
+
+
+if __name__ == "__main__" and os.environ.get("OUTPROJ"):
+    outproj_perf()

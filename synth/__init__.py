@@ -113,20 +113,20 @@ def get_config(cfg: int, reuse_ratio: float = 0.9) -> Config:
     """BASELINE.json configs 1..5 as concrete shapes."""
     if cfg == 1:
         return Config(1, "cfg1: 1 layer, 4q/1kv, d64, r=64 n=128 prefill + 4 decodes @256",
-                      Shapes(4, 1, 64, 1), SideSpec([64], [128]), SideSpec([255] * 4, [1] * 4))
+                      Shapes(4, 1, 64, 1, hidden=256), SideSpec([64], [128]), SideSpec([255] * 4, [1] * 4))
     if cfg == 2:
         return Config(2, "cfg2: Llama-3-8B attention (32q/8kv d128): 8k prefill + decode 64@4k",
-                      Shapes(32, 8, 128, 32), SideSpec([0], [8192]), SideSpec([4095] * 64, [1] * 64))
+                      Shapes(32, 8, 128, 32, hidden=4096), SideSpec([0], [8192]), SideSpec([4095] * 64, [1] * 64))
     if cfg == 3:
         r, n, c = _cfg3_lengths(reuse_ratio=reuse_ratio)
         return Config(3, "cfg3: multi-turn chat mix, 90% prefix hit, 4 prefills n~U[512,2048] + decode 128@U[2k,8k]",
-                      Shapes(32, 8, 128, 32), SideSpec(r, n), SideSpec([x - 1 for x in c], [1] * len(c)))
+                      Shapes(32, 8, 128, 32, hidden=4096), SideSpec(r, n), SideSpec([x - 1 for x in c], [1] * len(c)))
     if cfg == 4:
         return Config(4, "cfg4: Llama-3-70B attention (64q/8kv d128, hidden 8192): 8k prefill + decode 64@4k",
                       Shapes(64, 8, 128, 80, hidden=8192), SideSpec([0], [8192]), SideSpec([4095] * 64, [1] * 64))
     if cfg == 5:
         return Config(5, "cfg5: long context: 32k prefill + decode 256@2k",
-                      Shapes(32, 8, 128, 32), SideSpec([0], [32768]), SideSpec([2047] * 256, [1] * 256))
+                      Shapes(32, 8, 128, 32, hidden=4096), SideSpec([0], [32768]), SideSpec([2047] * 256, [1] * 256))
     raise ValueError(cfg)
 
 

@@ -1,0 +1,84 @@
+"""Multi-process (gloo, world_size 2, CPU) tests of the KV-head-sharded path's host logic:
+shard ranges, replicated page tables (hash all-gather), and that sharded attention + sharded
+out-projection + all-reduce reproduces the unsharded oracle result."""
+import math
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch.multiprocessing as mp
+
+from paper_2504_14489_b200 import shard
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def _worker(rank, world, port, q):
+    import torch
+    import torch.distributed as dist
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        import oracle
+        import synth
+        from synth import Shapes, SideSpec
+        from tests.helpers import oracle_build_side
+        Hq, Hkv, d, hidden = 8, 2, 64, 96
+        spec = SideSpec([40, 0], [30, 9])
+        full = synth.make_side(77, Shapes(Hq, Hkv, d, 1), spec, decode=False)
+        # each rank: its kv heads / q heads of the same seeded workload
+        ka, kb = shard.kv_head_range(rank, world, Hkv)
+        qa, qb = shard.q_head_range(rank, world, Hq, Hkv)
+        mine = synth.SideData(spec, full.q[:, qa:qb], [k[:, ka:kb] for k in full.k_rows],
+                              [v[:, ka:kb] for v in full.v_rows])
+        st = oracle_build_side(mine, 16, 5, kb - ka, d)
+        h = shard.page_table_hash(st["page_indptr"], st["page_ids"])
+        hs = [None] * world
+        dist.all_gather_object(hs, h)
+        o, _ = oracle.attention(mine.q, st["kpool"], st["vpool"], st["qo_indptr"], st["kv_len"],
+                                st["page_indptr"], st["page_ids"], 1 / math.sqrt(d))
+        g = np.random.default_rng(3)
+        wo = synth.f32_to_bf16_bits((g.standard_normal((Hq * d, hidden)) / 30).astype(np.float32))
+        ra, rb = shard.wo_row_range(rank, world, Hq, Hkv, d)
+        y = torch.from_numpy(oracle.outproj(o.reshape(o.shape[0], -1), wo[ra:rb]))
+        dist.all_reduce(y)
+        if rank == 0:
+            stf = oracle_build_side(full, 16, 5, Hkv, d)
+            of, _ = oracle.attention(full.q, stf["kpool"], stf["vpool"], stf["qo_indptr"], stf["kv_len"],
+                                     stf["page_indptr"], stf["page_ids"], 1 / math.sqrt(d))
+            yf = oracle.outproj(of.reshape(of.shape[0], -1), wo)
+            q.put((len(set(hs)), float(np.max(np.abs(y.numpy() - yf))), float(np.max(np.abs(of[:, qa:qb] - o)))))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_kv_head_sharded_layer_gloo():
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    ps = [ctx.Process(target=_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in ps:
+        p.start()
+    for p in ps:
+        p.join(120)
+    assert all(p.exitcode == 0 for p in ps)
+    n_hashes, dy, do = q.get(timeout=5)
+    assert n_hashes == 1            # identical page tables on both ranks
+    assert do == 0.0                # head-sharded attention == the same heads of the full one (bitwise)
+    assert dy < 1e-12               # sharded out-proj + all-reduce == unsharded O . W_o
+
+
+def test_shard_ranges():
+    assert shard.kv_head_range(1, 4, 8) == (2, 4)
+    assert shard.q_head_range(1, 4, 64, 8) == (16, 32)
+    assert shard.wo_row_range(3, 8, 64, 8, 128) == (24 * 128, 32 * 128)
+    with pytest.raises(ValueError):
+        shard.kv_head_range(0, 3, 8)
+    assert shard.page_table_hash([0, 2], [5, 7]) != shard.page_table_hash([0, 2], [7, 5])

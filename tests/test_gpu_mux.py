@@ -123,3 +123,58 @@ def test_run_layer_multi_layer_with_append(mux, part):
                               os_["page_indptr"], os_["page_ids"], 0.125)
     for layer in (0, 1):
         check_close(o[layer].cpu().numpy(), ref, what=f"layer {layer}")
+
+
+def test_run_layer_outproj_and_allreduce_hook(mux, part):
+    """a7 on the multiplexed path: each layer's out-projection runs on the side's partition and
+    the hook enqueues a (world-1) NCCL all-reduce of y on the same stream; y matches the
+    oracle's O . W_o (on the oracle's own attention output) within the bf16 output tolerance."""
+    import torch
+    from paper_2504_14489_b200 import nccl
+    import synth
+    Hq, Hkv, d, hidden = 8, 2, 128, 384
+    pf, dc, pool, g_pf, g_dc = _workload(mux, Hq, Hkv, d)
+    wo_bits = synth.make_wo(801, Shapes(Hq, Hkv, d, 1, hidden=hidden))
+    w_o = torch.from_numpy(wo_bits.view(np.int16)).cuda().view(torch.bfloat16)
+    comms = [nccl.Comm(0, 1), nccl.Comm(0, 1)]
+    calls = []
+
+    def hook_for(side, y):
+        def h(s, layer, stream):
+            assert s == side and stream != 0
+            calls.append((s, layer))
+            comms[side].all_reduce_(y, stream)
+        return h
+    try:
+        for split in (-1, 1):
+            ws = torch.empty(max(16, mux.mux_decode_workspace_bytes(3, Hq, d, 2)), dtype=torch.uint8, device="cuda")
+            o_pf = torch.empty((429, Hq, d), dtype=torch.bfloat16, device="cuda")
+            o_dc = torch.empty((3, Hq, d), dtype=torch.bfloat16, device="cuda")
+            y_pf = torch.full((429, hidden), float("nan"), dtype=torch.float32, device="cuda")
+            y_dc = torch.full((3, hidden), float("nan"), dtype=torch.float32, device="cuda")
+            s_pf = mux.make_side(g_pf["batch"], Hq, g_pf["q"], o_pf, scale=1 / math.sqrt(d),
+                                 w_o=w_o, y=y_pf, hook=hook_for(1, y_pf))
+            s_dc = mux.make_side(g_dc["batch"], Hq, g_dc["q"], o_dc, scale=1 / math.sqrt(d), num_splits=2, ws=ws,
+                                 w_o=w_o, y=y_dc, hook=hook_for(0, y_dc))
+            calls.clear()
+            mux.mux_run_layer(part, split, pool, s_pf, s_dc, None)
+            torch.cuda.synchronize()
+            assert sorted(calls) == [(0, 0), (1, 0)]
+            kimg = pool.k[0].view(torch.int16).cpu().numpy().view(np.uint16)
+            vimg = pool.v[0].view(torch.int16).cpu().numpy().view(np.uint16)
+            for side, g, o, y in ((pf, g_pf, o_pf, y_pf), (dc, g_dc, o_dc, y_dc)):
+                ref_o, _ = oracle.attention(side.q, kimg, vimg, g["qo_indptr"], g["kv_len"], g["page_indptr"],
+                                            g["page_ids"], 1 / math.sqrt(d))
+                # DESIGN.md R22: the out-projection consumes O in the activation dtype (bf16), so the
+                # oracle's Y is bf16(O_oracle) . W_o; R8's bound then covers the GPU's O rounding flips
+                o_bf16 = synth.f32_to_bf16_bits(ref_o.reshape(ref_o.shape[0], -1).astype(np.float32))
+                ref_y = oracle.outproj(o_bf16, wo_bits)
+                check_close(y.cpu().numpy(), ref_y, what=f"y split {split}")
+                # and bitwise equal to the standalone out-proj of the side's own o
+                y2 = torch.empty_like(y)
+                mux.mux_outproj(o.view(o.shape[0], -1), w_o, y2)
+                torch.cuda.synchronize()
+                assert torch.equal(y, y2)
+    finally:
+        for c in comms:
+            c.close()

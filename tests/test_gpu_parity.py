@@ -205,3 +205,45 @@ def test_prefill_v_range_flag(mux):
     torch.cuda.synchronize()
     assert gs2["pool"].error_flags(clear=True) & 1
     assert gs2["pool"].error_flags() == 0
+
+
+# ----------------------------------------------------------------------------- out-proj (a7)
+@pytest.mark.parametrize("T,K,N", [(64, 1024, 8192 // 8), (200, 256, 384), (1, 128, 256), (300, 512, 520),
+                                   (128, 4096, 4096), (33, 640, 200), (129, 256, 256), (96, 128, 8)])
+def test_outproj_parity(mux, T, K, N):
+    """Y = O . W_o partial GEMM vs the oracle's float64 product (O6); T <= 128 takes the skinny
+    (swap-AB) kernel, larger T the 128x256 tile kernel; ragged T / N tails on both."""
+    import torch
+    g = np.random.default_rng(T + K + N)
+    x = synth.f32_to_bf16_bits(g.standard_normal((T, K)).astype(np.float32))
+    w = synth.f32_to_bf16_bits((g.standard_normal((K, N)) / np.sqrt(K)).astype(np.float32))
+    ref = oracle.outproj(x, w)
+    xd = torch.from_numpy(x.view(np.int16)).cuda().view(torch.bfloat16)
+    wd = torch.from_numpy(w.view(np.int16)).cuda().view(torch.bfloat16)
+    y = torch.empty((T, N), dtype=torch.float32, device="cuda")
+    mux.mux_outproj(xd, wd, y)
+    yb = torch.empty((T, N), dtype=torch.bfloat16, device="cuda")
+    mux.mux_outproj(xd, wd, yb)
+    torch.cuda.synchronize()
+    check_close(y.cpu().numpy(), ref, atol=1e-4, rtol=1e-4, what="outproj f32")
+    check_close(yb.float().cpu().numpy(), ref, what="outproj bf16")
+
+
+def test_outproj_sharded_sum_equals_full(mux):
+    """KV-head sharding: sum over G shards of O_g W_o,g == O W_o (block identity)."""
+    import torch
+    g = np.random.default_rng(5)
+    T, Hq, d, hidden, G = 96, 16, 128, 512, 4
+    x = synth.f32_to_bf16_bits(g.standard_normal((T, Hq * d)).astype(np.float32))
+    w = synth.f32_to_bf16_bits((g.standard_normal((Hq * d, hidden)) / 40).astype(np.float32))
+    full = oracle.outproj(x, w)
+    acc = torch.zeros((T, hidden), dtype=torch.float32, device="cuda")
+    kk = Hq * d // G
+    for s in range(G):
+        xs = torch.from_numpy(np.ascontiguousarray(x[:, s * kk:(s + 1) * kk]).view(np.int16)).cuda().view(torch.bfloat16)
+        ws = torch.from_numpy(np.ascontiguousarray(w[s * kk:(s + 1) * kk]).view(np.int16)).cuda().view(torch.bfloat16)
+        y = torch.empty((T, hidden), dtype=torch.float32, device="cuda")
+        mux.mux_outproj(xs, ws, y)
+        acc += y
+    torch.cuda.synchronize()
+    check_close(acc.cpu().numpy(), full, atol=1e-4, rtol=1e-4, what="sharded outproj")
