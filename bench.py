@@ -148,8 +148,9 @@ class Workload:
         self.dc_o = torch.empty((Bd, self.Hq, self.d), dtype=torch.bfloat16, device=dev)
         # a7: this rank's rows of W_o (N(0, 1/(Hq d)), one matrix reused by every layer) and outputs
         self.hidden = S.hidden
-        self.w_o = (torch.randn((self.Hq * self.d, self.hidden), generator=g, device=dev) /
-                    math.sqrt(S.Hq * self.d)).to(torch.bfloat16)
+        w_o = (torch.randn((self.Hq * self.d, self.hidden), generator=g, device=dev) /
+               math.sqrt(S.Hq * self.d)).to(torch.bfloat16)
+        self.w_o = mux.mux_outproj_pack_w(w_o)  # weight prep (once, untimed): tile-packed layout
         self.pf_y = torch.empty((Tp, self.hidden), dtype=torch.bfloat16, device=dev)
         self.dc_y = torch.empty((Bd, self.hidden), dtype=torch.bfloat16, device=dev)
         self.hooks = {}

@@ -214,7 +214,8 @@ typedef struct {
   void* ws;                /* decode only */
   size_t ws_bytes;
   /* a7 (optional, w_o == NULL: off): after each layer's attention, y = o . w_o with
-   * o [total_q][Hq*d] bf16 (o_dtype must be bf16), w_o [Hq*d][hidden] bf16, y [total_q][hidden] */
+   * o [total_q][Hq*d] bf16 (o_dtype must be bf16), w_o = [Hq*d][hidden] bf16 PACKED by
+   * mux_outproj_pack_w (w_stride = packed bytes per layer, 0 = shared), y [total_q][hidden] */
   const void* w_o;
   void* y;
   int64_t w_stride, y_stride;
@@ -240,9 +241,23 @@ int mux_run_layer(mux_part_t part, int32_t split_idx, mux_pool_t pool,
                   mux_side_times* times, mux_stream_t join_stream);
 
 /* a7 building block (multi-GPU out-projection partial sums, P:702 TP): Y[T][N] (bf16 or
- * f32) = X[T][K] (bf16, row-major) . W[K][N] (bf16, row-major), fp32 accumulation. */
-int mux_outproj(const void* x, const void* w, void* y, int32_t y_dtype, int32_t T, int32_t K,
+ * f32) = X[T][K] (bf16, row-major) . W[K][N], fp32 accumulation.
+ *
+ * W is a weight: it is passed PACKED, once re-laid out by mux_outproj_pack_w into tiles of
+ * 128 columns x 64 rows (16 KiB each, in the 128-byte-swizzled image the tensor cores read),
+ * tile (nt, kb) at byte offset (nt * ceil(K/64) + kb) * 16384, zero-padded past K and N, so
+ * every stage of the GEMM is one contiguous 16 KiB bulk copy.
+ * Requirements: K and N multiples of 8; x, w_packed, y 16-byte aligned.  Deterministic
+ * (no atomics).  Errors: MUX_ERR_INVALID_ARG / MUX_ERR_UNSUPPORTED / MUX_ERR_CUDA. */
+int mux_outproj(const void* x, const void* w_packed, void* y, int32_t y_dtype, int32_t T, int32_t K,
                 int32_t N, mux_stream_t stream);
+
+/* bytes of the packed layout of a [K][N] weight: ceil(N/128) * ceil(K/64) * 16384 */
+size_t mux_outproj_packed_bytes(int32_t K, int32_t N);
+
+/* pack W [K][N] bf16 row-major (device) into w_packed (device, mux_outproj_packed_bytes),
+ * asynchronously on `stream`; bit-exact re-layout (plus zero padding). */
+int mux_outproj_pack_w(const void* w, void* w_packed, int32_t K, int32_t N, mux_stream_t stream);
 
 const char* mux_last_error(void);
 /* library version string, e.g. "mux-b200 0.1 sm_100a" */

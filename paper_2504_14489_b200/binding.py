@@ -91,6 +91,7 @@ def lib():
         "mux_partition_memory": [c_p, ctypes.POINTER(c_i64)],
         "mux_run_layer": [c_p, c_i32, c_p, ctypes.POINTER(SideC), ctypes.POINTER(SideC), c_p, c_p],
         "mux_outproj": [c_p, c_p, c_p, c_i32, c_i32, c_i32, c_i32, c_p],
+        "mux_outproj_pack_w": [c_p, c_p, c_i32, c_i32, c_p],
     }
     for name, args in sig.items():
         f = getattr(L, name)
@@ -98,6 +99,8 @@ def lib():
         f.restype = ctypes.c_int
     L.mux_decode_workspace_bytes.argtypes = [c_i32, c_i32, c_i32, c_i32]
     L.mux_decode_workspace_bytes.restype = c_sz
+    L.mux_outproj_packed_bytes.argtypes = [c_i32, c_i32]
+    L.mux_outproj_packed_bytes.restype = c_sz
     L.mux_decode_num_splits.argtypes = [c_i32, c_i32, c_i32, c_i32]
     L.mux_decode_num_splits.restype = c_i32
     L.mux_partition_configs.argtypes = [c_i32, c_i32, c_i32, c_p, c_i32]
@@ -291,14 +294,44 @@ def mux_num_prefill_layers(t_decode: float, t_prefill: float, n_layers_model: in
     return int(lib().mux_num_prefill_layers(t_decode, t_prefill, n_layers_model, remaining))
 
 
-def mux_outproj(x, w, y, stream=None):
-    """a7 partial GEMM: y[T][N] = x[T][K] . w[K][N] (bf16 in, fp32 accumulate, y bf16 or fp32)."""
+class PackedW:
+    """A [K][N] bf16 weight re-laid out by mux_outproj_pack_w (include/mux.h).  `data` is a
+    uint8 device tensor [layers][packed_bytes] (layers = 1 for a single matrix)."""
+
+    def __init__(self, data, K: int, N: int):
+        self.data, self.K, self.N = data, K, N
+
+    @property
+    def layer_bytes(self) -> int:
+        return int(self.data[0].numel())
+
+
+def mux_outproj_packed_bytes(K: int, N: int) -> int:
+    return int(lib().mux_outproj_packed_bytes(K, N))
+
+
+def mux_outproj_pack_w(w, stream=None) -> PackedW:
+    """Pack w [K][N] (or [layers][K][N]) bf16 for mux_outproj / mux_side.w_o."""
+    import torch
+    w3 = w if w.dim() == 3 else w.unsqueeze(0)
+    L_, K, N = w3.shape
+    nb = mux_outproj_packed_bytes(K, N)
+    out = torch.empty((L_, nb), dtype=torch.uint8, device=w.device)
+    for i in range(L_):
+        _check(lib().mux_outproj_pack_w(_ptr(w3[i].contiguous()), _ptr(out[i]), K, N, _stream(stream)))
+    return PackedW(out, K, N)
+
+
+def mux_outproj(x, w: PackedW, y, stream=None):
+    """a7 partial GEMM: y[T][N] = x[T][K] . W[K][N] (bf16 in, fp32 accumulate, y bf16 or fp32);
+    W packed by mux_outproj_pack_w."""
     import torch
     T, K = x.shape
-    K2, N = w.shape
-    assert K == K2 and tuple(y.shape) == (T, N)
+    assert isinstance(w, PackedW), "mux_outproj takes a PackedW (mux_outproj_pack_w)"
+    N = w.N
+    assert K == w.K and tuple(y.shape) == (T, N)
     yd = MUX_DTYPE_F32 if y.dtype == torch.float32 else MUX_DTYPE_BF16
-    _check(lib().mux_outproj(_ptr(x), _ptr(w), _ptr(y), yd, T, K, N, _stream(stream)))
+    _check(lib().mux_outproj(_ptr(x), _ptr(w.data), _ptr(y), yd, T, K, N, _stream(stream)))
 
 
 def mux_device_sm_count(device: int = 0) -> int:
@@ -366,10 +399,11 @@ def make_side(batch: Batch, num_q_heads: int, q, o, k_new=None, v_new=None, lse=
     s.ws = _ptr(ws)
     s.ws_bytes = ws.numel() * ws.element_size() if ws is not None else 0
     if w_o is not None:
-        s.w_o, s.y = _ptr(w_o), _ptr(y)
-        s.w_stride = w_o[0].numel() * w_o.element_size() if w_o.dim() == 3 else 0
+        assert isinstance(w_o, PackedW), "w_o must be packed (mux_outproj_pack_w)"
+        s.w_o, s.y = _ptr(w_o.data), _ptr(y)
+        s.w_stride = w_o.layer_bytes if w_o.data.shape[0] > 1 else 0
         s.y_stride = y[0].numel() * y.element_size() if y.dim() == 3 else 0
-        s.hidden = int(w_o.shape[-1])
+        s.hidden = int(w_o.N)
         s.y_dtype = MUX_DTYPE_F32 if y.dtype == torch.float32 else MUX_DTYPE_BF16
     cb = None
     if hook is not None:

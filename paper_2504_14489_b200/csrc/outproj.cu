@@ -6,18 +6,26 @@
 // output that an all-reduce completes.  This kernel is that per-GPU GEMM (bf16 in, fp32
 // accumulate in TMEM, bf16 or fp32 out); the all-reduce runs on the side's NCCL communicator.
 //
-// B200 design: one CTA per 128 x 256 output tile, 6 warps: warp 4 = TMA producer, warp 5 =
-// TMEM owner + single-thread tcgen05.mma issuer, warps 0-3 = epilogue (thread = output row).
-// 4-stage ring of {A: 128 rows x 64 k (K-major, SWIZZLE_128B), B: 64 k x 256 n (MN-major,
-// 4 boxes of 64 n)}, 48 KiB per stage; 4 MMAs (M=128, N=256, K=16) per stage; rows / columns
-// past T / N come from out-of-bounds TMA zero fill and are not stored.
+// W is a weight, so it is stored PACKED (mux_outproj_pack_w): 128 n x 64 k tiles of 16 KiB in
+// exactly the SWIZZLE_128B MN-major image tcgen05 reads (two 8 KiB halves of 64 n, row = k,
+// 16-byte chunk c of row k stored at chunk c ^ (k & 7)), tile (nt, kb) at (nt*KB + kb)*16 KiB.
+// Each pipeline stage's W operand is then one contiguous 16 KiB cp.async.bulk: the tensor-map
+// load of the row-major W fetched 128-byte rows 8 KiB apart and capped the skinny kernel at
+// ~40 GB/s per SM (ncu, profiles/r01_summary.md).
 //
-// Skinny variant (T <= 128, the decode side: one token per sequence): the 128-row M tile would
-// be mostly zero fill and N/256 CTAs too few to stream W_o at the partition's bandwidth, so the
-// kernel computes the transpose  Y^T = W^T . X^T  instead: M = 128 columns of W (A operand
-// MN-major, straight from W's row-major layout), N = T rounded up to 32 (B = X, K-major), one
-// CTA per 128 columns of W, 6-stage ring, stored directly from TMEM (no split-K: the
-// result stays bitwise deterministic).
+// Tile kernel (T > 128): one CTA per 128 x 256 output tile, 6 warps: warp 4 = producer (TMA for
+// X, bulk copies for W), warp 5 = TMEM owner + single-thread tcgen05.mma issuer, warps 0-3 =
+// epilogue (thread = output row).  4-stage ring of {A: X 128 rows x 64 k (K-major, TMA
+// SWIZZLE_128B), B: 2 packed W tiles = 64 k x 256 n (MN-major)}, 48 KiB per stage.
+//
+// Skinny kernel (T <= 128, the decode side: one token per sequence): the 128-row M tile would
+// be mostly zero fill, so it computes the transpose Y^T = W^T . X^T: M = 128 columns of W (A =
+// one packed tile, MN-major), N = T rounded up to 32 (B = X, K-major via TMA), one CTA per 128
+// columns of W, a ~200 KiB ring of 2-4 stages of ks k-blocks each (one ks x 16 KiB bulk copy of
+// W per stage), stored straight from TMEM (no split-K: bitwise deterministic).  Measured limit:
+// ~100 GB/s of smem fill per SM (bytes in flight / DRAM latency), so on a decode partition its
+// time is W + X-re-read bytes / (SMs x ~100 GB/s).
+// Rows / columns past T / N come from TMA zero fill or packing pads and are not stored.
 #include "pool.h"
 
 namespace mux {
@@ -25,6 +33,7 @@ namespace {
 
 constexpr int kGBM = 128, kGBN = 256, kGBK = 64, kGStages = 4;
 constexpr int kGThreads = 192;
+constexpr int kPackTile = 128 * kGBK * 2;  // 16 KiB
 
 struct GemmSmem {
   static constexpr int kA = kGBM * kGBK * 2;          // 16 KiB
@@ -37,12 +46,41 @@ struct GemmSmem {
 
 struct GemmParams {
   void* y;
+  const uint8_t* w_pk;
   int T, N, K, y_f32;
 };
 
+__device__ __forceinline__ void store_row32(const GemmParams& p, int row, int col, const uint32_t* v) {
+  if (row >= p.T) return;
+  if (p.y_f32) {
+    float* dst = static_cast<float*>(p.y) + static_cast<size_t>(row) * p.N + col;
+    if (col + 32 <= p.N && (p.N & 3) == 0) {
+#pragma unroll
+      for (int i = 0; i < 8; ++i)
+        reinterpret_cast<float4*>(dst)[i] = make_float4(__uint_as_float(v[4 * i]), __uint_as_float(v[4 * i + 1]),
+                                                        __uint_as_float(v[4 * i + 2]), __uint_as_float(v[4 * i + 3]));
+    } else {
+      for (int i = 0; i < 32 && col + i < p.N; ++i) dst[i] = __uint_as_float(v[i]);
+    }
+  } else {
+    uint16_t* dst = static_cast<uint16_t*>(p.y) + static_cast<size_t>(row) * p.N + col;
+    if (col + 32 <= p.N && (p.N & 7) == 0) {
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+        reinterpret_cast<uint4*>(dst)[i] =
+            make_uint4(dev::pack_bf16(__uint_as_float(v[8 * i]), __uint_as_float(v[8 * i + 1])),
+                       dev::pack_bf16(__uint_as_float(v[8 * i + 2]), __uint_as_float(v[8 * i + 3])),
+                       dev::pack_bf16(__uint_as_float(v[8 * i + 4]), __uint_as_float(v[8 * i + 5])),
+                       dev::pack_bf16(__uint_as_float(v[8 * i + 6]), __uint_as_float(v[8 * i + 7])));
+    } else {
+      for (int i = 0; i < 32 && col + i < p.N; ++i)
+        dst[i] = static_cast<uint16_t>(dev::pack_bf16(__uint_as_float(v[i]), 0.f) & 0xFFFFu);
+    }
+  }
+}
+
 __global__ void __launch_bounds__(kGThreads, 1)
-    outproj_kernel(const __grid_constant__ CUtensorMap tmap_x, const __grid_constant__ CUtensorMap tmap_w,
-                   const GemmParams p) {
+    outproj_kernel(const __grid_constant__ CUtensorMap tmap_x, const GemmParams p) {
   using L = GemmSmem;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -53,6 +91,9 @@ __global__ void __launch_bounds__(kGThreads, 1)
   const int warp = dev::warp_idx_uniform(), lane = threadIdx.x & 31;
   const int m0 = blockIdx.y * kGBM, n0 = blockIdx.x * kGBN;
   const int nk = (p.K + kGBK - 1) / kGBK;
+  const int ntiles = (p.N + 127) / 128;
+  const int nt0 = blockIdx.x * 2;
+  const bool second = nt0 + 1 < ntiles;  // N tail: the second 128-column tile may not exist
 
   if (threadIdx.x == 0) {
     for (int i = 0; i < 2 * kGStages + 1; ++i) dev::mbar_init(&full[i], 1);
@@ -67,17 +108,17 @@ __global__ void __launch_bounds__(kGThreads, 1)
   if (warp == 4) {
     if (lane == 0) {
       dev::tma_prefetch(&tmap_x);
-      dev::tma_prefetch(&tmap_w);
+      const uint8_t* w0 = p.w_pk + static_cast<size_t>(nt0) * nk * kPackTile;
+      const uint8_t* w1 = w0 + static_cast<size_t>(nk) * kPackTile;
       for (int kb = 0; kb < nk; ++kb) {
         const int s = kb % kGStages;
         if (kb >= kGStages) dev::mbar_wait_sleep(&empty[s], ((kb / kGStages) - 1) & 1);
-        dev::mbar_expect_tx(&full[s], L::kStage);
+        dev::mbar_expect_tx(&full[s], L::kA + (second ? 2 : 1) * kPackTile);
         uint8_t* a = smem + s * L::kStage;
         uint8_t* bt = a + L::kA;
         dev::tma_load_3d(a, &tmap_x, &full[s], kb * kGBK, m0, 0);
-#pragma unroll
-        for (int nb = 0; nb < kGBN / 64; ++nb)
-          dev::tma_load_3d(bt + nb * (kGBK * 128), &tmap_w, &full[s], n0 + nb * 64, kb * kGBK, 0);
+        dev::bulk_load(bt, w0 + static_cast<size_t>(kb) * kPackTile, kPackTile, &full[s]);
+        if (second) dev::bulk_load(bt + kPackTile, w1 + static_cast<size_t>(kb) * kPackTile, kPackTile, &full[s]);
       }
     }
   } else if (warp == 5) {
@@ -104,41 +145,13 @@ __global__ void __launch_bounds__(kGThreads, 1)
     dev::tc_fence_after();
     const int row = m0 + warp * 32 + lane;
     const uint32_t taddr = tmem + (static_cast<uint32_t>(warp * 32) << 16);
+    const int ncols = second ? kGBN : 128;
 #pragma unroll 1
-    for (int c = 0; c < kGBN / 32; ++c) {
+    for (int c = 0; c < ncols / 32; ++c) {
       uint32_t v[32];
       dev::tmem_ld32(taddr + c * 32, v);
       dev::tmem_wait_ld();
-      const int col = n0 + c * 32;
-      if (row < p.T) {
-        if (p.y_f32) {
-          float* dst = static_cast<float*>(p.y) + static_cast<size_t>(row) * p.N + col;
-          if (col + 32 <= p.N && (p.N & 3) == 0) {
-#pragma unroll
-            for (int i = 0; i < 8; ++i)
-              reinterpret_cast<float4*>(dst)[i] = make_float4(__uint_as_float(v[4 * i]), __uint_as_float(v[4 * i + 1]),
-                                                              __uint_as_float(v[4 * i + 2]), __uint_as_float(v[4 * i + 3]));
-          } else {
-            for (int i = 0; i < 32 && col + i < p.N; ++i) dst[i] = __uint_as_float(v[i]);
-          }
-        } else {
-          uint16_t* dst = static_cast<uint16_t*>(p.y) + static_cast<size_t>(row) * p.N + col;
-          if (col + 32 <= p.N && (p.N & 7) == 0) {
-#pragma unroll
-            for (int i = 0; i < 4; ++i)
-              reinterpret_cast<uint4*>(dst)[i] =
-                  make_uint4(dev::pack_bf16(__uint_as_float(v[8 * i]), __uint_as_float(v[8 * i + 1])),
-                             dev::pack_bf16(__uint_as_float(v[8 * i + 2]), __uint_as_float(v[8 * i + 3])),
-                             dev::pack_bf16(__uint_as_float(v[8 * i + 4]), __uint_as_float(v[8 * i + 5])),
-                             dev::pack_bf16(__uint_as_float(v[8 * i + 6]), __uint_as_float(v[8 * i + 7])));
-          } else {
-            for (int i = 0; i < 32 && col + i < p.N; ++i) {
-              const uint32_t pk = dev::pack_bf16(__uint_as_float(v[i]), 0.f);
-              dst[i] = static_cast<uint16_t>(pk & 0xFFFFu);
-            }
-          }
-        }
-      }
+      store_row32(p, row, n0 + c * 32, v);
     }
   }
   dev::tc_fence_before();
@@ -149,42 +162,44 @@ __global__ void __launch_bounds__(kGThreads, 1)
   }
 }
 
-constexpr int kSStages = 6;
+// ---------------------------------------------------------------- skinny (T <= 128)
+// stage = KS consecutive k-blocks: KS packed W tiles (ONE contiguous KS x 16 KiB bulk copy) +
+// KS X boxes of TN x 128 B; as many stages as fit ~200 KiB
+constexpr int kSMaxStages = 12;
+constexpr int kSkinnyRing = 200 * 1024;
 
-struct SkinnySmem {
-  static constexpr int kA = 128 * kGBK * 2;           // 16 KiB: 64 k x 128 n of W (2 boxes of 64 n)
-  static constexpr int kB = 128 * kGBK * 2;           // up to 128 t x 64 k of X
-  static constexpr int kStage = kA + kB;
-  static constexpr int kBar = kSStages * kStage;
-  static constexpr int kTmemSlot = kBar + (2 * kSStages + 1) * 8;
-  static constexpr int kBytes = kTmemSlot + 16;
-};
+__host__ __device__ inline int skinny_stage_bytes(int TN, int ks) { return ks * (kPackTile + TN * kGBK * 2); }
+__host__ __device__ inline int skinny_stages(int TN, int ks) {
+  const int s = kSkinnyRing / skinny_stage_bytes(TN, ks);
+  return s < kSMaxStages ? s : kSMaxStages;
+}
+constexpr int kSkinnySmemMax = kSkinnyRing + (2 * kSMaxStages + 1) * 8 + 16 + 1024;
 
 struct SkinnyParams {
   void* y;
-  int T, N, K, TN, kb_per_split, y_f32, atomic;
+  const uint8_t* w_pk;
+  int T, N, K, TN, ks, y_f32;
 };
 
 __global__ void __launch_bounds__(kGThreads, 1)
-    outproj_skinny_kernel(const __grid_constant__ CUtensorMap tmap_x, const __grid_constant__ CUtensorMap tmap_w,
-                          const SkinnyParams p) {
-  using L = SkinnySmem;
+    outproj_skinny_kernel(const __grid_constant__ CUtensorMap tmap_x, const SkinnyParams p) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  uint64_t* full = reinterpret_cast<uint64_t*>(smem + L::kBar);
-  uint64_t* empty = full + kSStages;
-  uint64_t* acc_full = empty + kSStages;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem + L::kTmemSlot);
+  const int ks = p.ks;
+  const int stage_bytes = skinny_stage_bytes(p.TN, ks), nst = skinny_stages(p.TN, ks);
+  const int x_off = ks * kPackTile;                      // X boxes follow the W tiles in a stage
+  const uint32_t x_box = static_cast<uint32_t>(p.TN) * kGBK * 2;
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + nst * stage_bytes);
+  uint64_t* empty = full + kSMaxStages;
+  uint64_t* acc_full = empty + kSMaxStages;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acc_full + 1);
   const int warp = dev::warp_idx_uniform(), lane = threadIdx.x & 31;
   const int n0 = blockIdx.x * 128;
-  const int nk_total = (p.K + kGBK - 1) / kGBK;
-  const int kb0 = blockIdx.y * p.kb_per_split;
-  const int kb1 = min(nk_total, kb0 + p.kb_per_split);
-  const int nk = kb1 - kb0;
-  const uint32_t b_bytes = static_cast<uint32_t>(p.TN) * kGBK * 2;
+  const int nk = (p.K + kGBK - 1) / kGBK;
+  const int nstage = (nk + ks - 1) / ks;
 
   if (threadIdx.x == 0) {
-    for (int i = 0; i < 2 * kSStages + 1; ++i) dev::mbar_init(&full[i], 1);
+    for (int i = 0; i < 2 * kSMaxStages + 1; ++i) dev::mbar_init(&full[i], 1);
     dev::fence_mbar_init();
   }
   if (warp == 5) dev::tmem_alloc(tmem_slot, 128);
@@ -196,37 +211,38 @@ __global__ void __launch_bounds__(kGThreads, 1)
   if (warp == 4) {
     if (lane == 0) {
       dev::tma_prefetch(&tmap_x);
-      dev::tma_prefetch(&tmap_w);
-      for (int i = 0; i < nk; ++i) {
-        const int s = i % kSStages, kb = kb0 + i;
-        if (i >= kSStages) dev::mbar_wait_sleep(&empty[s], ((i / kSStages) - 1) & 1);
-        dev::mbar_expect_tx(&full[s], L::kA + b_bytes);
-        uint8_t* a = smem + s * L::kStage;
-        dev::tma_load_3d(a, &tmap_w, &full[s], n0, kb * kGBK, 0);
-        dev::tma_load_3d(a + kGBK * 128, &tmap_w, &full[s], n0 + 64, kb * kGBK, 0);
-        dev::tma_load_3d(a + L::kA, &tmap_x, &full[s], kb * kGBK, 0, 0);
+      const uint8_t* wt = p.w_pk + static_cast<size_t>(blockIdx.x) * nk * kPackTile;
+      for (int i = 0; i < nstage; ++i) {
+        const int s = i % nst, kb = i * ks, cnt = min(ks, nk - kb);
+        if (i >= nst) dev::mbar_wait_sleep(&empty[s], ((i / nst) - 1) & 1);
+        dev::mbar_expect_tx(&full[s], cnt * (kPackTile + x_box));
+        uint8_t* a = smem + s * stage_bytes;
+        dev::bulk_load(a, wt + static_cast<size_t>(kb) * kPackTile, cnt * kPackTile, &full[s]);
+        for (int j = 0; j < cnt; ++j) dev::tma_load_3d(a + x_off + j * x_box, &tmap_x, &full[s], (kb + j) * kGBK, 0, 0);
       }
     }
   } else if (warp == 5) {
-    if (lane == 0 && nk > 0) {
+    if (lane == 0) {
       const uint32_t idesc = dev::umma_idesc_bf16(128, p.TN, 1, 0);
-      const uint64_t d0 = dev::umma_desc_sw128(dev::smem_u32(smem), kGBK * 128, 1024);      // A = W^T, MN-major
-      const uint64_t e0 = dev::umma_desc_sw128(dev::smem_u32(smem + L::kA), 16, 1024);      // B = X^T, K-major
-      for (int i = 0; i < nk; ++i) {
-        const int s = i % kSStages;
-        dev::mbar_wait_sleep(&full[s], (i / kSStages) & 1);
+      const uint64_t d0 = dev::umma_desc_sw128(dev::smem_u32(smem), kGBK * 128, 1024);       // A = W^T, MN-major
+      const uint64_t e0 = dev::umma_desc_sw128(dev::smem_u32(smem + x_off), 16, 1024);       // B = X^T, K-major
+      for (int i = 0; i < nstage; ++i) {
+        const int s = i % nst, cnt = min(ks, nk - i * ks);
+        dev::mbar_wait_sleep(&full[s], (i / nst) & 1);
         dev::tc_fence_after();
+        for (int j = 0; j < cnt; ++j)
 #pragma unroll
-        for (int kk = 0; kk < kGBK / 16; ++kk)
-          dev::umma_ss(tmem, d0 + ((s * L::kStage + kk * 16 * 128) >> 4), e0 + ((s * L::kStage + kk * 32) >> 4), idesc,
-                       (i > 0 || kk > 0) ? 1u : 0u);
+          for (int kk = 0; kk < kGBK / 16; ++kk)
+            dev::umma_ss(tmem, d0 + ((s * stage_bytes + j * kPackTile + kk * 16 * 128) >> 4),
+                         e0 + ((s * stage_bytes + j * x_box + kk * 32) >> 4), idesc, (i > 0 || j > 0 || kk > 0) ? 1u : 0u);
         dev::umma_commit(&empty[s]);
       }
       dev::umma_commit(acc_full);
     }
     __syncwarp();
-  } else if (nk > 0) {
-    // epilogue: TMEM lane = output column n0 + 32*warp + lane, TMEM column = token t
+  } else {
+    // epilogue: TMEM lane = output column n0 + 32*warp + lane, TMEM column = token t; a warp
+    // stores 32 consecutive columns of one token row per instruction
     dev::mbar_wait_sleep(acc_full, 0);
     dev::tc_fence_after();
     const int col = n0 + warp * 32 + lane;
@@ -243,9 +259,7 @@ __global__ void __launch_bounds__(kGThreads, 1)
           if (t < p.T) {
             const size_t off = static_cast<size_t>(t) * p.N + col;
             const float f = __uint_as_float(v[j]);
-            if (p.atomic)
-              atomicAdd(static_cast<float*>(p.y) + off, f);
-            else if (p.y_f32)
+            if (p.y_f32)
               static_cast<float*>(p.y)[off] = f;
             else
               static_cast<uint16_t*>(p.y)[off] = static_cast<uint16_t>(dev::pack_bf16(f, 0.f) & 0xFFFFu);
@@ -262,11 +276,48 @@ __global__ void __launch_bounds__(kGThreads, 1)
   }
 }
 
+// ---------------------------------------------------------------- weight packing
+// one thread per 16-byte chunk of the packed image: (tile, half, row k, stored chunk position)
+__global__ void pack_w_kernel(const uint16_t* __restrict__ w, uint4* __restrict__ out, int K, int N, int KB,
+                              size_t nchunks) {
+  for (size_t i = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; i < nchunks;
+       i += static_cast<size_t>(gridDim.x) * blockDim.x) {
+    const int pos = static_cast<int>(i & 7);           // stored chunk position within the 128 B row
+    const int k = static_cast<int>((i >> 3) & 63);      // row = k within the tile
+    const int half = static_cast<int>((i >> 9) & 1);    // n 0-63 / 64-127 of the tile
+    const size_t tile = i >> 10;                        // nt * KB + kb
+    const int kb = static_cast<int>(tile % KB), nt = static_cast<int>(tile / KB);
+    const int c = pos ^ (k & 7);                        // logical chunk (8 columns)
+    const int n = nt * 128 + half * 64 + c * 8, kk = kb * kGBK + k;
+    uint4 v = make_uint4(0, 0, 0, 0);
+    if (kk < K && n < N) v = *reinterpret_cast<const uint4*>(w + static_cast<size_t>(kk) * N + n);
+    out[i] = v;
+  }
+}
+
 }  // namespace
 }  // namespace mux
 
 using namespace mux;
 
+extern "C" size_t mux_outproj_packed_bytes(int32_t K, int32_t N) {
+  if (K < 1 || N < 1) return 0;
+  return static_cast<size_t>((N + 127) / 128) * ((K + kGBK - 1) / kGBK) * kPackTile;
+}
+
+extern "C" int mux_outproj_pack_w(const void* w, void* w_packed, int32_t K, int32_t N, mux_stream_t stream) {
+  if (!w || !w_packed) return fail(MUX_ERR_INVALID_ARG, "mux_outproj_pack_w: NULL pointer");
+  if (K < 1 || N < 1) return fail(MUX_ERR_INVALID_ARG, "mux_outproj_pack_w: K, N must be >= 1");
+  if (N % 8) return fail(MUX_ERR_UNSUPPORTED, "mux_outproj_pack_w: N must be a multiple of 8");
+  if ((reinterpret_cast<uintptr_t>(w) | reinterpret_cast<uintptr_t>(w_packed)) & 15)
+    return fail(MUX_ERR_INVALID_ARG, "mux_outproj_pack_w: pointers must be 16-byte aligned");
+  const size_t nchunks = mux_outproj_packed_bytes(K, N) / 16;
+  const int blocks = static_cast<int>(std::min<size_t>((nchunks + 255) / 256, 148 * 16));
+  pack_w_kernel<<<blocks, 256, 0, reinterpret_cast<cudaStream_t>(stream)>>>(
+      static_cast<const uint16_t*>(w), static_cast<uint4*>(w_packed), K, N, (K + kGBK - 1) / kGBK, nchunks);
+  MUX_CUDA(cudaGetLastError());
+  return MUX_OK;
+}
 
 extern "C" int mux_outproj(const void* x, const void* w, void* y, int32_t y_dtype, int32_t T, int32_t K, int32_t N,
                            mux_stream_t stream) {
@@ -276,45 +327,44 @@ extern "C" int mux_outproj(const void* x, const void* w, void* y, int32_t y_dtyp
   if ((K % 8) || (N % 8)) return fail(MUX_ERR_UNSUPPORTED, "mux_outproj: K and N must be multiples of 8");
   if ((reinterpret_cast<uintptr_t>(x) | reinterpret_cast<uintptr_t>(w) | reinterpret_cast<uintptr_t>(y)) & 15)
     return fail(MUX_ERR_INVALID_ARG, "mux_outproj: pointers must be 16-byte aligned");
-  // X [T][K] -> K-major A boxes {64 k, 128 rows}; W [K][N] -> MN-major B boxes {64 n, 64 k}
-  CUtensorMap tx, tw;
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  const uint8_t* wp = static_cast<const uint8_t*>(w);
+  // X [T][K] -> K-major boxes {64 k, rows}
+  CUtensorMap tx;
   uint64_t dx[3] = {static_cast<uint64_t>(K), static_cast<uint64_t>(T), 1};
   uint64_t sx[2] = {static_cast<uint64_t>(K) * 2, static_cast<uint64_t>(K) * T * 2};
+  if (T <= 128) {
+    const int TN = T <= 32 ? 32 : (T <= 64 ? 64 : 128);
+    uint32_t bx[3] = {kGBK, static_cast<uint32_t>(TN), 1};
+    int rc = make_tmap_bf16(&tx, x, 3, dx, sx, bx);
+    if (rc) return rc;
+    static bool attr_done = false;
+    if (!attr_done) {
+      MUX_CUDA(cudaFuncSetAttribute(outproj_skinny_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    kSkinnySmemMax));
+      attr_done = true;
+    }
+    // k-blocks per stage: the largest that still leaves >= 2 stages in the ring (fewer, bigger
+    // copies and barrier round trips: 17.6 us at ks 4 vs 22.3 at ks 2 and 31.5 at ks 1 for
+    // T=64, K=N=4096 on 32 CTAs, scripts/skinny_dbg.py)
+    const int ks = TN <= 64 ? 4 : 2;
+    SkinnyParams sp{y, wp, T, N, K, TN, ks, y_dtype == MUX_DTYPE_F32};
+    outproj_skinny_kernel<<<(N + 127) / 128, kGThreads, kSkinnySmemMax, st>>>(tx, sp);
+    MUX_CUDA(cudaGetLastError());
+    return MUX_OK;
+  }
   uint32_t bx[3] = {kGBK, kGBM, 1};
   int rc = make_tmap_bf16(&tx, x, 3, dx, sx, bx);
   if (rc) return rc;
-  uint64_t dw[3] = {static_cast<uint64_t>(N), static_cast<uint64_t>(K), 1};
-  uint64_t sw[2] = {static_cast<uint64_t>(N) * 2, static_cast<uint64_t>(N) * K * 2};
-  uint32_t bw[3] = {64, kGBK, 1};
-  if ((rc = make_tmap_bf16(&tw, w, 3, dw, sw, bw))) return rc;
   static bool attr_done = false;
   const int smem = GemmSmem::kBytes + 1024;
   if (!attr_done) {
     MUX_CUDA(cudaFuncSetAttribute(outproj_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
     attr_done = true;
   }
-  if (T <= 128) {
-    const int TN = T <= 32 ? 32 : (T <= 64 ? 64 : 128);
-    uint32_t bxs[3] = {kGBK, static_cast<uint32_t>(TN), 1};
-    if ((rc = make_tmap_bf16(&tx, x, 3, dx, sx, bxs))) return rc;
-    static bool sk_attr_done = false;
-    const int ssm = SkinnySmem::kBytes + 1024;
-    if (!sk_attr_done) {
-      MUX_CUDA(cudaFuncSetAttribute(outproj_skinny_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, ssm));
-      sk_attr_done = true;
-    }
-    const int nk = (K + kGBK - 1) / kGBK;
-    const int ntiles = (N + 127) / 128;
-    // split = 1: deterministic (atomic split-K would break the mux == isolated bitwise identity)
-    const int split = 1, per = nk;
-    SkinnyParams sp{y, T, N, K, TN, per, y_dtype == MUX_DTYPE_F32, 0};
-    outproj_skinny_kernel<<<dim3(ntiles, split), kGThreads, ssm, reinterpret_cast<cudaStream_t>(stream)>>>(tx, tw, sp);
-    MUX_CUDA(cudaGetLastError());
-    return MUX_OK;
-  }
-  GemmParams prm{y, T, N, K, y_dtype == MUX_DTYPE_F32};
+  GemmParams prm{y, wp, T, N, K, y_dtype == MUX_DTYPE_F32};
   dim3 grid((N + kGBN - 1) / kGBN, (T + kGBM - 1) / kGBM);
-  outproj_kernel<<<grid, kGThreads, smem, reinterpret_cast<cudaStream_t>(stream)>>>(tx, tw, prm);
+  outproj_kernel<<<grid, kGThreads, smem, st>>>(tx, prm);
   MUX_CUDA(cudaGetLastError());
   return MUX_OK;
 }

@@ -79,11 +79,12 @@ if __name__ == "__main__":
 
 
 def outproj_perf():
-    for T, K, N in ((8192, 4096, 4096), (64, 4096, 4096), (8192, 1024, 8192)):
+    for T, K, N in ((8192, 4096, 4096), (64, 4096, 4096), (128, 8192, 8192), (8192, 1024, 8192), (8192, 8192, 8192)):
         x = torch.randn((T, K), device="cuda").to(torch.bfloat16)
         w = (torch.randn((K, N), device="cuda") / 64).to(torch.bfloat16)
+        wp = mux.mux_outproj_pack_w(w)
         y = torch.empty((T, N), device="cuda", dtype=torch.bfloat16)
-        t = timed(lambda: mux.mux_outproj(x, w, y), iters=10)
+        t = timed(lambda: mux.mux_outproj(x, wp, y), iters=10)
         ref = (x.float() @ w.float())
         err = (y.float() - ref).abs().max().item()
         tb = timed(lambda: torch.matmul(x, w), iters=10)

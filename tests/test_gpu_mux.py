@@ -135,7 +135,7 @@ def test_run_layer_outproj_and_allreduce_hook(mux, part):
     Hq, Hkv, d, hidden = 8, 2, 128, 384
     pf, dc, pool, g_pf, g_dc = _workload(mux, Hq, Hkv, d)
     wo_bits = synth.make_wo(801, Shapes(Hq, Hkv, d, 1, hidden=hidden))
-    w_o = torch.from_numpy(wo_bits.view(np.int16)).cuda().view(torch.bfloat16)
+    w_o = mux.mux_outproj_pack_w(torch.from_numpy(wo_bits.view(np.int16)).cuda().view(torch.bfloat16))
     comms = [nccl.Comm(0, 1), nccl.Comm(0, 1)]
     calls = []
 

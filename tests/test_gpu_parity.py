@@ -219,7 +219,7 @@ def test_outproj_parity(mux, T, K, N):
     w = synth.f32_to_bf16_bits((g.standard_normal((K, N)) / np.sqrt(K)).astype(np.float32))
     ref = oracle.outproj(x, w)
     xd = torch.from_numpy(x.view(np.int16)).cuda().view(torch.bfloat16)
-    wd = torch.from_numpy(w.view(np.int16)).cuda().view(torch.bfloat16)
+    wd = mux.mux_outproj_pack_w(torch.from_numpy(w.view(np.int16)).cuda().view(torch.bfloat16))
     y = torch.empty((T, N), dtype=torch.float32, device="cuda")
     mux.mux_outproj(xd, wd, y)
     yb = torch.empty((T, N), dtype=torch.bfloat16, device="cuda")
@@ -241,9 +241,32 @@ def test_outproj_sharded_sum_equals_full(mux):
     kk = Hq * d // G
     for s in range(G):
         xs = torch.from_numpy(np.ascontiguousarray(x[:, s * kk:(s + 1) * kk]).view(np.int16)).cuda().view(torch.bfloat16)
-        ws = torch.from_numpy(np.ascontiguousarray(w[s * kk:(s + 1) * kk]).view(np.int16)).cuda().view(torch.bfloat16)
+        ws = mux.mux_outproj_pack_w(
+            torch.from_numpy(np.ascontiguousarray(w[s * kk:(s + 1) * kk]).view(np.int16)).cuda().view(torch.bfloat16))
         y = torch.empty((T, hidden), dtype=torch.float32, device="cuda")
         mux.mux_outproj(xs, ws, y)
         acc += y
     torch.cuda.synchronize()
     check_close(acc.cpu().numpy(), full, atol=1e-4, rtol=1e-4, what="sharded outproj")
+
+
+@pytest.mark.parametrize("K,N", [(64, 128), (200, 264), (4096, 4096)])
+def test_outproj_pack_layout(mux, K, N):
+    """The packed weight image equals the documented layout (include/mux.h), computed here
+    element by element with numpy: tile (nt, kb) at (nt*KB + kb)*16 KiB, half h = n-block of
+    64, row k, 16-byte chunk c stored at c ^ (k & 7); zero padding past K and N."""
+    import torch
+    g = np.random.default_rng(K * N)
+    w = g.integers(0, 65536, size=(K, N), dtype=np.uint16)
+    pk = mux.mux_outproj_pack_w(torch.from_numpy(w.view(np.int16)).cuda().view(torch.bfloat16))
+    torch.cuda.synchronize()
+    got = pk.data[0].cpu().numpy().view(np.uint16)
+    KB, NT = (K + 63) // 64, (N + 127) // 128
+    assert got.size * 2 == mux.mux_outproj_packed_bytes(K, N) == NT * KB * 16384
+    wp = np.zeros((KB * 64, NT * 128), np.uint16)
+    wp[:K, :N] = w
+    # [nt][kb][h][k][pos][8]: element (k, n = nt*128 + h*64 + (pos ^ (k&7))*8 + e)
+    nt, kb, h, k, pos, e = np.meshgrid(np.arange(NT), np.arange(KB), np.arange(2), np.arange(64), np.arange(8),
+                                       np.arange(8), indexing="ij")
+    want = wp[kb * 64 + k, nt * 128 + h * 64 + (pos ^ (k & 7)) * 8 + e].reshape(-1)
+    np.testing.assert_array_equal(got, want)
