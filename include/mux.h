@@ -148,7 +148,10 @@ int mux_prefill_attn(mux_pool_t pool, int32_t layer, const mux_batch* batch, int
 
 /* a4 + a5: decode split-KV paged attention followed (num_splits > 1) by the
  * log-sum-exp split combine.  q: device bf16 [num_seqs][Hq][d]; o, lse as prefill.
- * num_splits: 0 = auto (mux_decode_num_splits for this device's SM count).
+ * num_splits: 0 = auto (mux_decode_num_splits for this device's SM count).  Splits are
+ * BALANCED: every split covers C = ceil(ceil(max_kv/16) / num_splits) pages of its sequence,
+ * so a sequence of p pages uses ceil(p/C) splits (the longest uses num_splits) and every CTA
+ * carries the same work; a ragged batch does not leave SMs idle behind its longest sequence.
  * ws: device workspace of >= mux_decode_workspace_bytes(num_seqs, Hq, d, num_splits)
  * bytes (may be NULL when the resolved num_splits is 1). */
 int mux_decode_attn(mux_pool_t pool, int32_t layer, const mux_batch* batch, int32_t num_q_heads,

@@ -43,6 +43,7 @@ struct DecodeParams {
   const int32_t* page_indptr;
   const int32_t* page_ids;
   int num_splits, hq, hkv, g;
+  int pages_per_split;       // C: every split of every sequence covers <= C pages (balanced units)
   int page_row0;             // layer * num_pages (TMA page coordinate offset)
   int o_f32;
   float scale_log2;
@@ -86,10 +87,14 @@ __global__ void __launch_bounds__(kDecodeThreads, 1)
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int kv_len = __ldg(p.kv_len + b);
   const int npages = (kv_len + kPage - 1) / kPage;
-  const int pps = (npages + p.num_splits - 1) / p.num_splits;
+  // balanced split-KV: a fixed chunk of C pages per split for EVERY sequence, so all CTAs carry
+  // (at most) the same work; a sequence shorter than the longest uses fewer splits and its
+  // surplus CTAs exit at once (the combine recomputes the split count from kv_len).
+  const int pps = p.pages_per_split;
   const int pg0 = min(npages, split * pps);
-  const int pg1 = min(npages, pg0 + pps);
+  const int pg1 = split == p.num_splits - 1 ? npages : min(npages, pg0 + pps);  // last split: the rest
   const int n_my = pg1 - pg0;
+  if (split > 0 && n_my <= 0) return;
   const int* ptab = p.page_ids + __ldg(p.page_indptr + b);
 
   if (threadIdx.x == 0) {
@@ -320,16 +325,20 @@ __global__ void __launch_bounds__(kDecodeThreads, 1)
 template <int D>
 __global__ void __launch_bounds__(D) combine_kernel(const float* __restrict__ part_o, const float* __restrict__ part_m,
                                                     const float* __restrict__ part_l, void* o, float* lse,
+                                                    const int32_t* __restrict__ kv_len, int hq, int pages_per_split,
                                                     int num_splits, int o_f32) {
   const size_t row = blockIdx.x;  // b*Hq + h
   const int c = threadIdx.x;
+  // splits this sequence actually used (the others exited without writing partials)
+  const int npages = (__ldg(kv_len + row / hq) + kPage - 1) / kPage;
+  const int used = max(1, min(num_splits, (npages + pages_per_split - 1) / pages_per_split));
   float M = -INFINITY;
-  for (int s = 0; s < num_splits; ++s) {
+  for (int s = 0; s < used; ++s) {
     const float l = part_l[row * num_splits + s];
     if (l > 0.f) M = fmaxf(M, part_m[row * num_splits + s]);
   }
   float W = 0.f, acc = 0.f;
-  for (int s = 0; s < num_splits; ++s) {
+  for (int s = 0; s < used; ++s) {
     const float l = part_l[row * num_splits + s];
     if (!(l > 0.f)) continue;
     const float w = l * dev::ex2(part_m[row * num_splits + s] - M);
@@ -356,8 +365,8 @@ int launch_decode_hg(mux_pool* pool, const DecodeParams& prm, int B, cudaStream_
   kern<<<grid, kDecodeThreads, smem, st>>>(pool->tmap_kg, pool->tmap_vg, prm);
   MUX_CUDA(cudaGetLastError());
   if (prm.num_splits > 1) {
-    combine_kernel<D><<<B * prm.hq, D, 0, st>>>(prm.part_o, prm.part_m, prm.part_l, prm.o, prm.lse,
-                                                prm.num_splits, prm.o_f32);
+    combine_kernel<D><<<B * prm.hq, D, 0, st>>>(prm.part_o, prm.part_m, prm.part_l, prm.o, prm.lse, prm.kv_len,
+                                                prm.hq, prm.pages_per_split, prm.num_splits, prm.o_f32);
     MUX_CUDA(cudaGetLastError());
   }
   return MUX_OK;
@@ -435,6 +444,10 @@ int mux_decode_attn(mux_pool_t pool, int32_t layer, const mux_batch* b, int32_t 
   prm.page_indptr = b->page_indptr;
   prm.page_ids = b->page_ids;
   prm.num_splits = num_splits;
+  {
+    const int max_pages = (b->max_kv + kPage - 1) / kPage;
+    prm.pages_per_split = std::max(1, (max_pages + num_splits - 1) / num_splits);
+  }
   prm.hq = hq;
   prm.hkv = hkv;
   prm.g = g;

@@ -90,7 +90,7 @@ DECODE_CASES = [
 ]
 
 
-@pytest.mark.parametrize("splits", [1, 3, 0])
+@pytest.mark.parametrize("splits", [1, 3, 7, 0])
 @pytest.mark.parametrize("case", range(len(DECODE_CASES)))
 def test_decode_parity(mux, case, splits):
     d, Hq, Hkv, ctx = DECODE_CASES[case]
