@@ -190,7 +190,8 @@ class Workload:
     def sides(self, part_sms_dec: int, iters: int):
         mux = self.mux
         import torch
-        ns = mux.mux_decode_num_splits(self.dc_spec.num_seqs, self.Hkv, max(self.dc_spec.L), part_sms_dec)
+        ns = mux.mux_decode_num_splits(self.dc_spec.num_seqs, self.Hkv, max(self.dc_spec.L), part_sms_dec,
+                                       self.dc_spec.L, self.d)
         wsb = mux.mux_decode_workspace_bytes(self.dc_spec.num_seqs, self.Hq, self.d, ns)
         if self.ws is None or self.ws.numel() < wsb:
             self.ws = torch.empty(max(16, wsb), dtype=torch.uint8, device="cuda")

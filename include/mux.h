@@ -159,9 +159,13 @@ int mux_decode_attn(mux_pool_t pool, int32_t layer, const mux_batch* batch, int3
                     int32_t num_splits, void* ws, size_t ws_bytes, mux_stream_t stream);
 size_t mux_decode_workspace_bytes(int32_t num_seqs, int32_t num_q_heads, int32_t head_dim,
                                   int32_t num_splits);
-/* host heuristic: splits so that num_seqs*Hkv*splits CTAs fill `num_sms` SMs, capped by
- * the pages of the longest sequence */
-int32_t mux_decode_num_splits(int32_t num_seqs, int32_t num_kv_heads, int32_t max_kv, int32_t num_sms);
+/* host split-count choice for the balanced split-KV: simulates the launch (every split covers
+ * C = ceil(ceil(max_kv/16)/S) pages; CTAs of ~4 us start-up + ~100 GB/s streaming dispatched in
+ * launch order onto `num_sms` SMs; + the combine pass when S > 1) for S in {1,2,3,4,6,...,64}
+ * and returns the S of smallest predicted time.  kv_len: host array of the batch's contexts
+ * (NULL = every sequence at max_kv).  Pure host function. */
+int32_t mux_decode_num_splits(int32_t num_seqs, int32_t num_kv_heads, int32_t head_dim, const int32_t* kv_len,
+                              int32_t max_kv, int32_t num_sms);
 
 /* ------------------------------------------------------------------------------------
  * SM partitions (a6).  P:473: GreenContext binds streams to SM sets, reconfiguration

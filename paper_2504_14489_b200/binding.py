@@ -101,7 +101,7 @@ def lib():
     L.mux_decode_workspace_bytes.restype = c_sz
     L.mux_outproj_packed_bytes.argtypes = [c_i32, c_i32]
     L.mux_outproj_packed_bytes.restype = c_sz
-    L.mux_decode_num_splits.argtypes = [c_i32, c_i32, c_i32, c_i32]
+    L.mux_decode_num_splits.argtypes = [c_i32, c_i32, c_i32, c_p, c_i32, c_i32]
     L.mux_decode_num_splits.restype = c_i32
     L.mux_partition_configs.argtypes = [c_i32, c_i32, c_i32, c_p, c_i32]
     L.mux_partition_configs.restype = c_i32
@@ -277,8 +277,12 @@ def mux_decode_workspace_bytes(num_seqs: int, num_q_heads: int, head_dim: int, n
     return int(lib().mux_decode_workspace_bytes(num_seqs, num_q_heads, head_dim, num_splits))
 
 
-def mux_decode_num_splits(num_seqs: int, num_kv_heads: int, max_kv: int, num_sms: int) -> int:
-    return int(lib().mux_decode_num_splits(num_seqs, num_kv_heads, max_kv, num_sms))
+def mux_decode_num_splits(num_seqs: int, num_kv_heads: int, max_kv: int, num_sms: int, kv_len=None,
+                          head_dim: int = 128) -> int:
+    """Balanced split-KV split count (include/mux.h); kv_len = the batch's contexts (host)."""
+    a = _np32(kv_len) if kv_len is not None else None
+    return int(lib().mux_decode_num_splits(num_seqs, num_kv_heads, head_dim, a.ctypes.data if a is not None else None,
+                                           max_kv, num_sms))
 
 
 def mux_partition_configs(total_sms: int, granularity: int = 16, min_side: int = 12) -> List[int]:

@@ -23,6 +23,10 @@
 //   the normalised output, otherwise fp32 partials (o, m, l) for the combine kernel.
 #include <math.h>
 
+#include <algorithm>
+#include <queue>
+#include <vector>
+
 #include "pool.h"
 
 namespace mux {
@@ -396,21 +400,63 @@ size_t mux_decode_workspace_bytes(int32_t num_seqs, int32_t hq, int32_t d, int32
   return rows * d * 4 + rows * 8 + 256;
 }
 
-int32_t mux_decode_num_splits(int32_t num_seqs, int32_t hkv, int32_t max_kv, int32_t num_sms) {
+int32_t mux_decode_num_splits(int32_t num_seqs, int32_t hkv, int32_t head_dim, const int32_t* kv_len,
+                              int32_t max_kv, int32_t num_sms) {
   if (num_seqs < 1 || hkv < 1 || max_kv < 1) return 1;
   if (num_sms < 1) num_sms = 148;
+  if (head_dim < 1) head_dim = 128;
   int hg = 1;
   for (int c = 1; c <= 8; ++c)
     if (hkv % c == 0) hg = c;
-  const int64_t ctas = static_cast<int64_t>(num_seqs) * (hkv / hg);   // CTAs per split (1 CTA / SM)
-  const int64_t target = static_cast<int64_t>(num_sms) * 2;           // >= 2 waves
-  int64_t s = (target + ctas - 1) / ctas;
-  const int64_t pages = (max_kv + kPage - 1) / kPage;
-  const int64_t cap = pages / 8 > 1 ? pages / 8 : 1;                   // >= 8 pages per split
-  if (s > cap) s = cap;
-  if (s > 64) s = 64;
-  if (s < 1) s = 1;
-  return static_cast<int32_t>(s);
+  const int groups = hkv / hg;
+  const int max_pages = (max_kv + kPage - 1) / kPage;
+  // Host model of one launch (constants from B200 measurements, profiles/r01_summary.md): a CTA
+  // streams ~100 GB/s of K+V pages, costs ~4 us to start and drain, an empty CTA ~0.3 us; the
+  // combine pass ~6 us + its partial traffic.  The grid's CTAs are dispatched in launch order
+  // (split fastest) onto the first free SM; the split count with the smallest predicted
+  // makespan wins.  Balanced splits: C = ceil(max_pages / S) pages per split for every sequence.
+  const double page_us = static_cast<double>(hg) * kPage * head_dim * 2 * 2 / 1.0e5;
+  const double cta_us = 4.0, empty_us = 0.3;
+  std::vector<int> pages(num_seqs);
+  for (int i = 0; i < num_seqs; ++i) {
+    const int L = kv_len ? kv_len[i] : max_kv;
+    pages[i] = (std::max(L, 1) + kPage - 1) / kPage;
+  }
+  int64_t total_pages = 0;
+  for (int p : pages) total_pages += p;
+  // ~6.5 TB/s measured copy bandwidth (MEASURED_PEAKS hbm_gbs), in bytes per us
+  const double hbm_floor_us = static_cast<double>(total_pages) * groups * page_us * 1.0e5 / 6.5e6;
+  static const int cands[] = {1, 2, 3, 4, 6, 8, 12, 16, 24, 32, 48, 64};
+  int best_s = 1;
+  double best_t = 1e300;
+  std::vector<double> sm;
+  for (int S : cands) {
+    if (S > 1 && S > max_pages) break;
+    const int64_t ctas = static_cast<int64_t>(num_seqs) * groups * S;
+    if (S > 1 && ctas > 16LL * num_sms) break;     // finer units cannot pay for themselves
+    const int C = (max_pages + S - 1) / S;
+    sm.assign(std::min<int64_t>(num_sms, ctas), 0.0);
+    std::priority_queue<double, std::vector<double>, std::greater<double>> q(sm.begin(), sm.end());
+    double span = 0.0;
+    for (int b = 0; b < num_seqs; ++b)
+      for (int gi = 0; gi < groups; ++gi)
+        for (int sp = 0; sp < S; ++sp) {
+          const int p0 = sp * C;
+          const int np = sp == S - 1 ? std::max(0, pages[b] - p0) : std::max(0, std::min(C, pages[b] - p0));
+          const double t = (np > 0 || sp == 0) ? cta_us + np * page_us : empty_us;
+          const double st = q.top();
+          q.pop();
+          q.push(st + t);
+          span = std::max(span, st + t);
+        }
+    span = std::max(span, hbm_floor_us);  // the chip's HBM bandwidth caps any SM count
+    if (S > 1) span += 6.0 + static_cast<double>(num_seqs) * hkv * 8 * S * (head_dim + 2) * 4 / (num_sms * 1.0e5);
+    if (span < best_t * 0.98) {  // a finer split must win by > 2% (model noise)
+      best_t = span;
+      best_s = S;
+    }
+  }
+  return best_s;
 }
 
 int mux_decode_attn(mux_pool_t pool, int32_t layer, const mux_batch* b, int32_t hq, const void* q, void* o,
@@ -426,7 +472,8 @@ int mux_decode_attn(mux_pool_t pool, int32_t layer, const mux_batch* b, int32_t 
   if (!q || !o) return fail(MUX_ERR_INVALID_ARG, "q/o NULL");
   if (o_dtype != MUX_DTYPE_BF16 && o_dtype != MUX_DTYPE_F32) return fail(MUX_ERR_INVALID_ARG, "bad o_dtype");
   if (reinterpret_cast<uintptr_t>(q) & 15) return fail(MUX_ERR_INVALID_ARG, "q must be 16-byte aligned");
-  if (num_splits <= 0) num_splits = mux_decode_num_splits(b->num_seqs, hkv, b->max_kv, device_sm_count());
+  if (num_splits <= 0)
+    num_splits = mux_decode_num_splits(b->num_seqs, hkv, d, b->h_kv_len, b->max_kv, device_sm_count());
   if (num_splits > 1) {
     if (!ws || ws_bytes < mux_decode_workspace_bytes(b->num_seqs, hq, d, num_splits))
       return fail(MUX_ERR_WORKSPACE, "decode workspace missing or too small");

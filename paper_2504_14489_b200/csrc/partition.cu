@@ -170,7 +170,7 @@ static int run_side(mux_pool_t pool, const mux_side* s, bool decode, int sms, cu
   if (decode) {
     splits = s->num_splits > 0 ? s->num_splits
                                : mux_decode_num_splits(s->batch->num_seqs, pool->desc.num_kv_heads,
-                                                       s->batch->max_kv, sms);
+                                                       pool->desc.head_dim, s->batch->h_kv_len, s->batch->max_kv, sms);
   }
   for (int i = 0; i < s->num_layers; ++i) {
     const int layer = (s->layer0 + i) % nl;

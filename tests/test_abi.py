@@ -130,9 +130,17 @@ def test_n_pl_matches_paper_formula(mux):
 
 
 def test_decode_split_heuristic_and_workspace(mux):
-    assert mux.mux_decode_num_splits(64, 8, 4096, 148) == 5
-    assert mux.mux_decode_num_splits(4, 1, 256, 148) == 2          # capped at pages/8
-    assert mux.mux_decode_num_splits(1, 1, 16, 148) == 1
+    # launch-simulation choice (include/mux.h): uniform batches that already fill the SMs
+    # stay unsplit; one long sequence spreads over the SMs; a ragged batch splits finer than a
+    # uniform one of the same size; the count is capped at 64
+    f = mux.mux_decode_num_splits
+    assert f(64, 8, 4096, 32, [4096] * 64) == 1
+    assert f(64, 8, 4096, 16, [4096] * 64) == 1
+    assert f(1, 8, 4096, 32, [4096]) == 32
+    assert f(1, 1, 16, 148) == 1
+    assert f(1, 1, 1 << 20, 148) == 64
+    ragged = [1024 + (i * 997) % 7168 for i in range(48)]
+    assert f(48, 8, max(ragged), 32, ragged) > f(48, 8, max(ragged), 32, [max(ragged)] * 48)
     assert mux.mux_decode_workspace_bytes(64, 32, 128, 1) == 0
     assert mux.mux_decode_workspace_bytes(2, 4, 64, 3) >= 2 * 4 * 3 * (64 + 2) * 4
 

@@ -94,7 +94,7 @@ def test_fullsize_sampled_parity(mux, part, cfg, split):
 
     # ---- the bench's launch: one mux_run_layer on `split`, append + attention + out-projection
     dsms = part.query(split)[0]
-    ns = mux.mux_decode_num_splits(B, Hkv, max(L_dc), dsms)
+    ns = mux.mux_decode_num_splits(B, Hkv, max(L_dc), dsms, L_dc, d)
     ws = torch.empty(max(16, mux.mux_decode_workspace_bytes(B, Hq, d, ns)), dtype=torch.uint8, device="cuda")
     w_pk = mux.mux_outproj_pack_w(_to_dev(wo))
     o_pf = torch.empty((pf_spec.total_new, Hq, d), dtype=torch.bfloat16, device="cuda")

@@ -44,7 +44,7 @@ def _run(mux, side, Hq, Hkv, d, decode, num_pages=None, seed=11, o_f32=True, num
     o = torch.empty((T, Hq, d), dtype=torch.float32 if o_f32 else torch.bfloat16, device="cuda")
     lse = torch.empty((T, Hq), dtype=torch.float32, device="cuda")
     if decode:
-        ns = num_splits or mux.mux_decode_num_splits(side.spec.num_seqs, Hkv, max(side.spec.L), 148)
+        ns = num_splits or mux.mux_decode_num_splits(side.spec.num_seqs, Hkv, max(side.spec.L), 148, side.spec.L, d)
         wsb = mux.mux_decode_workspace_bytes(side.spec.num_seqs, Hq, d, ns)
         ws = torch.empty(max(wsb, 16), dtype=torch.uint8, device="cuda")
         mux.mux_decode_attn(gs["pool"], 0, gs["batch"], Hq, gs["q"], o, lse, scale=scale, num_splits=ns, ws=ws)
