@@ -266,6 +266,82 @@ size_t mux_outproj_packed_bytes(int32_t K, int32_t N);
  * asynchronously on `stream`; bit-exact re-layout (plus zero padding). */
 int mux_outproj_pack_w(const void* w, void* w_packed, int32_t K, int32_t N, mux_stream_t stream);
 
+/* ------------------------------------------------------------------------------------
+ * f1: bubble-less multiplex ENGINE above mux_run_layer.
+ * PAPER: layer-wise prefill ("splits the prefill phase into layers (PLs) ... can
+ * launch enough PBs to occupy compute resources for prefill, and return in time before the
+ * decode phase finishes"), decode-first launching, query-based synchronisation
+ * ("periodically polls CUDA events ... the corresponding prefill request is
+ * immediately merged into the current decode batch"), decode-termination hand-off of the
+ * later prefill layers to the freed SMs, best-fit decode SMs from worst-case
+ * estimates and N_PL = ceil(T_d * N_T / T_P).
+ *
+ * One host thread drives both sides.  A decode ITERATION = all N_T layers of the current
+ * decode batch (append of the new token + attention + out-projection per layer); it is
+ * launched when the previous one has completed (its tokens must return to the host before
+ * the next iteration), after retiring finished requests and merging completed
+ * prefills.  A prefill GROUP = N_PL consecutive layers of the active prefill batch; the engine
+ * keeps up to two groups queued on the prefill stream so the prefill SMs never drain.  When
+ * the decode batch is empty the remaining prefill layers go to the whole GPU.
+ * Activations are synthetic: token t of request j uses row (src_base_j + t) % src_rows of
+ * src_q / src_k / src_v (the QKV projections are outside this hot path).
+ * ---------------------------------------------------------------------------------- */
+typedef struct mux_engine* mux_engine_t;
+
+typedef struct {
+  int32_t num_q_heads;          /* Hq; Hkv, d and N_T (= pool num_layers) come from the pool */
+  float scale;
+  const void* src_q;            /* device bf16 [src_rows][Hq][d] */
+  const void* src_k;            /* device bf16 [src_rows][Hkv][d] */
+  const void* src_v;
+  int32_t src_rows;
+  const void* w_o;              /* packed W_o (mux_outproj_pack_w), NULL = no out-projection */
+  int32_t hidden;
+  int32_t max_decode_seqs;      /* decode batch capacity */
+  int32_t max_prefill_tokens;   /* cap on sum n of one prefill batch (>= the longest prompt) */
+  int32_t fixed_split;          /* >= -1: always this split (-1 = whole GPU, time-sliced sides);
+                                   -2: best-fit by the cost model below */
+  int32_t n_cost;               /* entries of the cost arrays (= partition split count) */
+  const double* dec_theta;      /* [n_cost][3] Eq.2 per split, us per layer (NULL: no model) */
+  const double* pf_theta;       /* [n_cost][4] Eq.1 per split, us per layer */
+  const double* dec_slowdown;   /* [n_cost] contention guard max slowdown, NULL = 1 */
+  double tbt_slo_us;            /* decode iteration target for the best-fit rule */
+  int32_t fixed_pl;             /* > 0: layers per prefill group instead of N_PL */
+  int32_t handoff;              /* 1: decode termination hands the prefill to the whole GPU */
+  int32_t keep_pages;           /* 1: finished requests keep their pages (for inspection) */
+} mux_engine_desc;
+
+typedef struct {
+  int32_t id;
+  int32_t cached;               /* r: prefix tokens already in the pool (preloaded at admission) */
+  int32_t prompt;               /* n >= 1: new prompt tokens (prefill) */
+  int32_t gen;                  /* decode iterations after the prefill (>= 0) */
+  int32_t src_base;
+} mux_request;
+
+typedef struct {
+  double makespan_us;           /* first to last engine kernel, device clock */
+  int64_t prefill_tokens, decode_tokens;
+  int32_t decode_iters, prefill_groups, split_changes, handoffs;
+  double busy_dec_us, busy_pf_us;
+  double bubble_ratio;          /* R21: idle share of each side's [first, last] window, averaged */
+  double bubble_ratio_dec, bubble_ratio_pf;
+  double tbt_mean_us, tbt_max_us; /* decode iteration end-to-end intervals */
+  double ttft_mean_us, ttft_max_us;
+} mux_engine_stats;
+
+int mux_engine_create(mux_engine_t* out, mux_part_t part, mux_pool_t pool, const mux_engine_desc* desc);
+/* queue requests (FCFS); all are considered to arrive at the start of mux_engine_run */
+int mux_engine_submit(mux_engine_t eng, const mux_request* reqs, int32_t n);
+/* run until every submitted request has finished its decode; blocks the calling thread */
+int mux_engine_run(mux_engine_t eng, mux_engine_stats* stats);
+/* a finished request's final context length and page table (needs keep_pages) */
+int mux_engine_request_pages(mux_engine_t eng, int32_t id, int32_t* kv_len, int32_t* page_ids, int32_t cap,
+                             int32_t* n_pages);
+/* per-iteration trace: for decode iteration i, out[i] = {split, batch size, start, end (ns)} */
+int mux_engine_trace(mux_engine_t eng, int64_t* out, int32_t cap, int32_t* n);
+int mux_engine_destroy(mux_engine_t eng);
+
 const char* mux_last_error(void);
 /* library version string, e.g. "mux-b200 0.1 sm_100a" */
 const char* mux_version(void);

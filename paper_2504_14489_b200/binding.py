@@ -54,6 +54,29 @@ class SideC(ctypes.Structure):
                 ("hook_user", c_p)]
 
 
+class EngineDesc(ctypes.Structure):
+    _fields_ = [("num_q_heads", c_i32), ("scale", c_f32), ("src_q", c_p), ("src_k", c_p), ("src_v", c_p),
+                ("src_rows", c_i32), ("w_o", c_p), ("hidden", c_i32), ("max_decode_seqs", c_i32),
+                ("max_prefill_tokens", c_i32), ("fixed_split", c_i32), ("n_cost", c_i32), ("dec_theta", c_p),
+                ("pf_theta", c_p), ("dec_slowdown", c_p), ("tbt_slo_us", c_dbl), ("fixed_pl", c_i32),
+                ("handoff", c_i32), ("keep_pages", c_i32)]
+
+
+class RequestC(ctypes.Structure):
+    _fields_ = [("id", c_i32), ("cached", c_i32), ("prompt", c_i32), ("gen", c_i32), ("src_base", c_i32)]
+
+
+class EngineStats(ctypes.Structure):
+    _fields_ = [("makespan_us", c_dbl), ("prefill_tokens", c_i64), ("decode_tokens", c_i64),
+                ("decode_iters", c_i32), ("prefill_groups", c_i32), ("split_changes", c_i32), ("handoffs", c_i32),
+                ("busy_dec_us", c_dbl), ("busy_pf_us", c_dbl), ("bubble_ratio", c_dbl), ("bubble_ratio_dec", c_dbl),
+                ("bubble_ratio_pf", c_dbl), ("tbt_mean_us", c_dbl), ("tbt_max_us", c_dbl), ("ttft_mean_us", c_dbl),
+                ("ttft_max_us", c_dbl)]
+
+    def as_dict(self):
+        return {k: getattr(self, k) for k, _ in self._fields_}
+
+
 class SideTimes(ctypes.Structure):
     _fields_ = [("dec_start_ns", c_u64), ("dec_end_ns", c_u64), ("pf_start_ns", c_u64), ("pf_end_ns", c_u64)]
 
@@ -92,6 +115,12 @@ def lib():
         "mux_run_layer": [c_p, c_i32, c_p, ctypes.POINTER(SideC), ctypes.POINTER(SideC), c_p, c_p],
         "mux_outproj": [c_p, c_p, c_p, c_i32, c_i32, c_i32, c_i32, c_p],
         "mux_outproj_pack_w": [c_p, c_p, c_i32, c_i32, c_p],
+        "mux_engine_create": [ctypes.POINTER(c_p), c_p, c_p, ctypes.POINTER(EngineDesc)],
+        "mux_engine_submit": [c_p, ctypes.POINTER(RequestC), c_i32],
+        "mux_engine_run": [c_p, ctypes.POINTER(EngineStats)],
+        "mux_engine_request_pages": [c_p, c_i32, ctypes.POINTER(c_i32), c_p, c_i32, ctypes.POINTER(c_i32)],
+        "mux_engine_trace": [c_p, c_p, c_i32, ctypes.POINTER(c_i32)],
+        "mux_engine_destroy": [c_p],
     }
     for name, args in sig.items():
         f = getattr(L, name)
@@ -423,3 +452,77 @@ def mux_run_layer(part: Partition, split_idx: int, pool: Pool, prefill: Optional
     _check(lib().mux_run_layer(part.h, split_idx, pool.h, ctypes.byref(prefill) if prefill is not None else None,
                                ctypes.byref(decode) if decode is not None else None, _ptr(times),
                                _stream(join_stream)))
+
+
+# ------------------------------------------------------------------------------ engine (f1)
+class Engine:
+    """The bubble-less multiplex engine (include/mux.h).  src_q/k/v: device
+    bf16 source rows of the synthetic activations; cost: optional costmodel.CostModel (per split
+    fits in partition order) for best-fit splits and N_PL."""
+
+    def __init__(self, part: "Partition", pool: Pool, num_q_heads: int, src_q, src_k, src_v, *,
+                 scale: float, w_o: "PackedW" = None, max_decode_seqs: int = 256,
+                 max_prefill_tokens: int = 16384, fixed_split: int = -2, cost=None, tbt_slo_us: float = 1e30,
+                 fixed_pl: int = 0, handoff: bool = True, keep_pages: bool = False):
+        d = EngineDesc()
+        d.num_q_heads, d.scale = num_q_heads, scale
+        d.src_q, d.src_k, d.src_v = _ptr(src_q), _ptr(src_k), _ptr(src_v)
+        d.src_rows = int(src_q.shape[0])
+        if w_o is not None:
+            d.w_o, d.hidden = _ptr(w_o.data), int(w_o.N)
+        d.max_decode_seqs, d.max_prefill_tokens = max_decode_seqs, max_prefill_tokens
+        d.fixed_split, d.tbt_slo_us, d.fixed_pl = fixed_split, tbt_slo_us, fixed_pl
+        d.handoff, d.keep_pages = int(handoff), int(keep_pages)
+        self._keep = [src_q, src_k, src_v, w_o]
+        if cost is not None:
+            n = part.n
+            dec = np.zeros((n, 3))
+            pf = np.zeros((n, 4))
+            sl = np.ones(n)
+            for i in range(n):
+                ds, ps, _, _ = part.query(i)
+                dec[i] = cost.decode[ds].theta
+                pf[i] = cost.prefill[ps].theta
+                sl[i] = cost.max_slowdown_dec.get(ds, 1.0)
+            self._cost = (np.ascontiguousarray(dec), np.ascontiguousarray(pf), np.ascontiguousarray(sl))
+            d.n_cost = n
+            d.dec_theta, d.pf_theta, d.dec_slowdown = (a.ctypes.data for a in self._cost)
+        self.desc = d
+        h = c_p()
+        _check(lib().mux_engine_create(ctypes.byref(h), part.h, pool.h, ctypes.byref(d)))
+        self.h = h
+
+    def submit(self, reqs):
+        """reqs: iterable of (id, cached, prompt, gen, src_base)."""
+        arr = (RequestC * len(reqs))(*[RequestC(*r) for r in reqs])
+        _check(lib().mux_engine_submit(self.h, arr, len(reqs)))
+
+    def run(self) -> dict:
+        st = EngineStats()
+        _check(lib().mux_engine_run(self.h, ctypes.byref(st)))
+        return st.as_dict()
+
+    def request_pages(self, rid: int):
+        kv, n = c_i32(), c_i32()
+        _check(lib().mux_engine_request_pages(self.h, rid, ctypes.byref(kv), None, 0, ctypes.byref(n)))
+        out = np.zeros(max(1, n.value), np.int32)
+        _check(lib().mux_engine_request_pages(self.h, rid, ctypes.byref(kv), out.ctypes.data, n.value, ctypes.byref(n)))
+        return kv.value, [int(x) for x in out[:n.value]]
+
+    def trace(self):
+        n = c_i32()
+        _check(lib().mux_engine_trace(self.h, None, 0, ctypes.byref(n)))
+        out = np.zeros((max(1, n.value), 6), np.int64)
+        _check(lib().mux_engine_trace(self.h, out.ctypes.data, n.value, ctypes.byref(n)))
+        return out[:n.value]
+
+    def close(self):
+        if getattr(self, "h", None):
+            lib().mux_engine_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass

@@ -1,0 +1,726 @@
+// f1: bubble-less multiplex engine above mux_run_layer's building blocks (include/mux.h).
+//
+// PAPER: P:529-531 layer-wise prefill ("PLs": launch enough prefill layers to keep the
+// prefill SMs busy and return before the decode iteration finishes; switch the later
+// prefill layers to the freed SMs when the decode batch terminates), P:535-537 query-based
+// synchronisation (poll CUDA events; merge a finished prefill into the decode batch at once),
+// P:498 decode launched first, P:657 best-fit decode SMs from worst-case estimates
+// (solo prediction x the contention guard's max slowdown)
+// N_PL = ceil(T_d N_T / T_P).
+//
+// B200 design: one host thread, no locks.  The device work of a decode iteration / prefill
+// group is exactly what mux_run_layer enqueues for one side (mux::run_side: append + attention
+// (+ combine) + out-projection per layer), on the green-context streams of the current split.
+// Batches are rebuilt on the host (page tables grow by one page every 16 decode tokens),
+// staged in pinned memory and copied with the iteration on its own stream; activations are
+// gathered from the caller's synthetic source rows by a copy kernel.  Every iteration and
+// group is bracketed by %globaltimer stamps in a device log, from which the run's bubble
+// ratio, TBT and TTFT are computed after the run (no profiler, no host clocks).
+#include <algorithm>
+#include <cmath>
+#include <deque>
+#include <thread>
+#include <vector>
+
+#include "pool.h"
+
+namespace mux {
+namespace {
+
+__global__ void gather_rows_kernel(const uint4* __restrict__ src, uint4* __restrict__ dst,
+                                   const int32_t* __restrict__ idx, int rows, int vec_per_row) {
+  const size_t n = static_cast<size_t>(rows) * vec_per_row;
+  for (size_t i = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<size_t>(gridDim.x) * blockDim.x) {
+    const size_t r = i / vec_per_row, c = i % vec_per_row;
+    dst[i] = src[static_cast<size_t>(__ldg(idx + r)) * vec_per_row + c];
+  }
+}
+
+int gather(const void* src, void* dst, const int32_t* idx, int rows, int row_bytes, cudaStream_t st) {
+  if (rows <= 0) return MUX_OK;
+  const int vec = row_bytes / 16;
+  const int blocks = static_cast<int>(std::min<size_t>((static_cast<size_t>(rows) * vec + 255) / 256, 1184));
+  gather_rows_kernel<<<blocks, 256, 0, st>>>(static_cast<const uint4*>(src), static_cast<uint4*>(dst), idx, rows,
+                                            vec);
+  MUX_CUDA(cudaGetLastError());
+  return MUX_OK;
+}
+
+struct Req {
+  mux_request r{};
+  std::vector<int32_t> pages;
+  int ctx = 0;          // tokens in the pool (kv_len after the last append)
+  int gen_left = 0;
+  int ttft_log = -1;    // log slot of the end stamp of its last prefill group
+  bool finished = false;
+};
+
+// one staging slot of a side: pinned host arrays + their device copy
+struct Slot {
+  int32_t* h = nullptr;
+  int32_t* d = nullptr;
+  size_t cap = 0;       // int32 entries
+  cudaEvent_t done = nullptr;
+  bool used = false;
+};
+
+struct Group {
+  cudaEvent_t ev;
+  bool last;
+  std::vector<int> reqs;
+};
+
+struct Interval {
+  int side;             // 0 decode, 1 prefill
+  int log;              // index of the start stamp; end = log + 1
+  int split, batch;
+};
+
+double eq2(const double* th, double sum_r, int bs) { return th[0] * sum_r + th[1] * bs + th[2]; }
+double eq1(const double* th, double sum_n2, double sum_nr, double sum_n) {
+  return th[0] * sum_n2 + th[1] * sum_nr + th[2] * sum_n + th[3];
+}
+
+}  // namespace
+}  // namespace mux
+
+struct mux_engine {
+  mux_part_t part = nullptr;
+  mux_pool_t pool = nullptr;
+  mux_engine_desc desc{};
+  std::vector<double> dec_theta, pf_theta, slowdown;
+  std::vector<mux::Req> reqs;
+  int Hkv = 0, d = 0, NT = 0;
+  // device buffers
+  void *dq = nullptr, *dk = nullptr, *dv = nullptr, *do_ = nullptr, *dy = nullptr, *ws = nullptr;
+  size_t ws_bytes = 0;
+  void *pq[2] = {}, *pk[2] = {}, *pv[2] = {}, *po[2] = {}, *py[2] = {};
+  void *prek = nullptr, *prev = nullptr;
+  int cap_dec = 0, cap_pf = 0, cap_pre = 0;
+  mux::Slot dslot[2], pslot[2], preslot[2];
+  unsigned long long* log = nullptr;
+  int log_cap = 0, log_n = 0;
+  std::vector<mux::Interval> iv;
+  std::vector<cudaEvent_t> events;
+  bool ran = false;
+};
+
+using namespace mux;
+
+namespace {
+
+int slot_reserve(Slot& s, size_t n) {
+  if (s.cap >= n) return MUX_OK;
+  if (s.h) cudaFreeHost(s.h);
+  if (s.d) cudaFree(s.d);
+  s.h = nullptr;
+  s.d = nullptr;
+  MUX_CUDA(cudaMallocHost(&s.h, n * 4));
+  MUX_CUDA(cudaMalloc(&s.d, n * 4));
+  if (!s.done) MUX_CUDA(cudaEventCreateWithFlags(&s.done, cudaEventDisableTiming));
+  s.cap = n;
+  return MUX_OK;
+}
+
+// the staging buffer may be rewritten only after the copy that read it has run
+int slot_acquire(Slot& s) {
+  if (s.used) MUX_CUDA(cudaEventSynchronize(s.done));
+  s.used = false;
+  return MUX_OK;
+}
+
+int new_event(mux_engine* e, cudaEvent_t* ev) {
+  MUX_CUDA(cudaEventCreateWithFlags(ev, cudaEventDisableTiming));
+  e->events.push_back(*ev);
+  return MUX_OK;
+}
+
+int log_pair(mux_engine* e, int* idx) {
+  if (e->log_n + 2 > e->log_cap) return fail(MUX_ERR_INVALID_ARG, "engine log full");
+  *idx = e->log_n;
+  e->log_n += 2;
+  return MUX_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+int mux_engine_create(mux_engine_t* out, mux_part_t part, mux_pool_t pool, const mux_engine_desc* desc) {
+  if (!out || !part || !pool || !desc) return fail(MUX_ERR_INVALID_ARG, "mux_engine_create: NULL argument");
+  *out = nullptr;
+  const int Hkv = pool->desc.num_kv_heads, d = pool->desc.head_dim;
+  if (desc->num_q_heads < Hkv || desc->num_q_heads % Hkv) return fail(MUX_ERR_UNSUPPORTED, "Hq must be a multiple of Hkv");
+  if (!desc->src_q || !desc->src_k || !desc->src_v || desc->src_rows < 1)
+    return fail(MUX_ERR_INVALID_ARG, "engine needs src_q/src_k/src_v rows");
+  if (desc->max_decode_seqs < 1 || desc->max_prefill_tokens < 1) return fail(MUX_ERR_INVALID_ARG, "engine capacities");
+  if (desc->w_o && desc->hidden < 8) return fail(MUX_ERR_INVALID_ARG, "hidden < 8 with w_o");
+  const int nsplit = mux_partition_count(part);
+  if (desc->fixed_split < -2 || desc->fixed_split >= nsplit) return fail(MUX_ERR_INVALID_ARG, "fixed_split out of range");
+  const bool model = desc->dec_theta && desc->pf_theta;
+  if (desc->fixed_split == -2 && (!model || desc->n_cost != nsplit))
+    return fail(MUX_ERR_INVALID_ARG, "best-fit split needs a cost model with one entry per split");
+  auto* e = new mux_engine();
+  e->part = part;
+  e->pool = pool;
+  e->desc = *desc;
+  e->Hkv = Hkv;
+  e->d = d;
+  e->NT = pool->desc.num_layers;
+  if (model) {
+    e->dec_theta.assign(desc->dec_theta, desc->dec_theta + 3 * desc->n_cost);
+    e->pf_theta.assign(desc->pf_theta, desc->pf_theta + 4 * desc->n_cost);
+    e->slowdown.assign(desc->n_cost, 1.0);
+    if (desc->dec_slowdown) e->slowdown.assign(desc->dec_slowdown, desc->dec_slowdown + desc->n_cost);
+  }
+  e->desc.dec_theta = e->desc.pf_theta = e->desc.dec_slowdown = nullptr;
+  *out = e;
+  return MUX_OK;
+}
+
+int mux_engine_submit(mux_engine_t e, const mux_request* rq, int32_t n) {
+  if (!e || n < 0 || (n > 0 && !rq)) return fail(MUX_ERR_INVALID_ARG, "mux_engine_submit: bad argument");
+  for (int i = 0; i < n; ++i) {
+    if (rq[i].prompt < 1 || rq[i].cached < 0 || rq[i].gen < 0)
+      return fail(MUX_ERR_INVALID_ARG, "request needs prompt >= 1, cached >= 0, gen >= 0");
+    if (rq[i].prompt > e->desc.max_prefill_tokens) return fail(MUX_ERR_INVALID_ARG, "prompt > max_prefill_tokens");
+    Req r;
+    r.r = rq[i];
+    e->reqs.push_back(r);
+  }
+  return MUX_OK;
+}
+
+static int engine_alloc(mux_engine* e) {
+  const int Hq = e->desc.num_q_heads, d = e->d, Hkv = e->Hkv;
+  int64_t tot_pages = 0, max_pre = 0, iters = 0;
+  for (auto& r : e->reqs) {
+    tot_pages += (r.r.cached + r.r.prompt + r.r.gen + kPage - 1) / kPage;
+    max_pre += r.r.cached;
+    iters += r.r.gen;
+  }
+  e->cap_dec = e->desc.max_decode_seqs;
+  e->cap_pf = e->desc.max_prefill_tokens;
+  e->cap_pre = static_cast<int>(std::max<int64_t>(1, max_pre));
+  const size_t qrow = static_cast<size_t>(Hq) * d * 2, kvrow = static_cast<size_t>(Hkv) * d * 2;
+  MUX_CUDA(cudaMalloc(&e->dq, e->cap_dec * qrow));
+  MUX_CUDA(cudaMalloc(&e->dk, e->cap_dec * kvrow));
+  MUX_CUDA(cudaMalloc(&e->dv, e->cap_dec * kvrow));
+  MUX_CUDA(cudaMalloc(&e->do_, e->cap_dec * qrow));
+  if (e->desc.w_o) MUX_CUDA(cudaMalloc(&e->dy, static_cast<size_t>(e->cap_dec) * e->desc.hidden * 2));
+  e->ws_bytes = mux_decode_workspace_bytes(e->cap_dec, Hq, d, 64);
+  MUX_CUDA(cudaMalloc(&e->ws, std::max<size_t>(e->ws_bytes, 256)));
+  for (int i = 0; i < 2; ++i) {
+    MUX_CUDA(cudaMalloc(&e->pq[i], e->cap_pf * qrow));
+    MUX_CUDA(cudaMalloc(&e->pk[i], e->cap_pf * kvrow));
+    MUX_CUDA(cudaMalloc(&e->pv[i], e->cap_pf * kvrow));
+    MUX_CUDA(cudaMalloc(&e->po[i], e->cap_pf * qrow));
+    if (e->desc.w_o) MUX_CUDA(cudaMalloc(&e->py[i], static_cast<size_t>(e->cap_pf) * e->desc.hidden * 2));
+  }
+  MUX_CUDA(cudaMalloc(&e->prek, e->cap_pre * kvrow));
+  MUX_CUDA(cudaMalloc(&e->prev, e->cap_pre * kvrow));
+  const size_t nreq = e->reqs.size();
+  for (int i = 0; i < 2; ++i) {
+    int rc = slot_reserve(e->dslot[i], 4 * static_cast<size_t>(e->cap_dec) + 8 + tot_pages);
+    if (!rc) rc = slot_reserve(e->pslot[i], 4 * nreq + 8 + tot_pages + e->cap_pf);
+    if (!rc) rc = slot_reserve(e->preslot[i], 4 * nreq + 8 + tot_pages + e->cap_pre);
+    if (rc) return rc;
+  }
+  e->log_cap = static_cast<int>(2 * (iters + static_cast<int64_t>(e->NT) * nreq + 64));
+  MUX_CUDA(cudaMalloc(&e->log, static_cast<size_t>(e->log_cap) * 8));
+  return MUX_OK;
+}
+
+// host arrays of a batch in a slot: [qo (B+1)][kv (B)][pind (B+1)][idx rows][page ids]
+struct Built {
+  mux_batch b{};
+  int32_t* d_idx = nullptr;
+  int rows = 0;
+  size_t n = 0;
+};
+
+static Built build_batch(Slot& s, const std::vector<Req*>& rs, const std::vector<int>& n_new,
+                         const std::vector<int>& kv, const std::vector<int>& pos0, int src_rows) {
+  Built out;
+  const int B = static_cast<int>(rs.size());
+  int32_t* qo = s.h;
+  int32_t* kl = qo + B + 1;
+  int32_t* pi = kl + B;
+  int32_t* idx = pi + B + 1;
+  int rows = 0;
+  for (int i = 0; i < B; ++i) rows += n_new[i];
+  int32_t* pids = idx + rows;
+  qo[0] = 0;
+  pi[0] = 0;
+  int max_q = 0, max_kv = 0, r = 0, pg = 0;
+  for (int i = 0; i < B; ++i) {
+    qo[i + 1] = qo[i] + n_new[i];
+    kl[i] = kv[i];
+    const int np = (kv[i] + kPage - 1) / kPage;
+    for (int p = 0; p < np; ++p) pids[pg++] = rs[i]->pages[p];
+    pi[i + 1] = pg;
+    for (int t = 0; t < n_new[i]; ++t) idx[r++] = static_cast<int32_t>((static_cast<int64_t>(rs[i]->r.src_base) + pos0[i] + t) % src_rows);
+    max_q = std::max(max_q, n_new[i]);
+    max_kv = std::max(max_kv, kv[i]);
+  }
+  out.n = static_cast<size_t>(pids + pg - s.h);
+  mux_batch& b = out.b;
+  b.num_seqs = B;
+  b.qo_indptr = s.d;
+  b.kv_len = s.d + B + 1;
+  b.page_indptr = s.d + 2 * B + 1;
+  b.page_ids = s.d + 3 * B + 2 + rows;
+  b.total_q = rows;
+  b.max_q = max_q;
+  b.max_kv = max_kv;
+  b.h_qo_indptr = qo;
+  b.h_kv_len = kl;
+  b.h_page_indptr = pi;
+  b.h_page_ids = pids;
+  out.d_idx = s.d + 3 * B + 2;
+  out.rows = rows;
+  return out;
+}
+
+int mux_engine_run(mux_engine_t e, mux_engine_stats* st) {
+  if (!e) return fail(MUX_ERR_INVALID_ARG, "engine NULL");
+  if (e->ran) return fail(MUX_ERR_INVALID_ARG, "mux_engine_run may be called once per engine");
+  e->ran = true;
+  int rc = engine_alloc(e);
+  if (rc) return rc;
+  const mux_engine_desc& D = e->desc;
+  const int Hq = D.num_q_heads, d = e->d, NT = e->NT, Hkv = e->Hkv;
+  const size_t qrow = static_cast<size_t>(Hq) * d * 2, kvrow = static_cast<size_t>(Hkv) * d * 2;
+  const int nsplit = mux_partition_count(e->part);
+  std::deque<int> queue;
+  for (int i = 0; i < static_cast<int>(e->reqs.size()); ++i) {
+    e->reqs[i].gen_left = e->reqs[i].r.gen;
+    queue.push_back(i);
+  }
+  std::vector<int> decode, ready;
+  std::deque<Group> pf_out;
+  struct Job {
+    bool active = false;
+    std::vector<int> reqs;
+    int layers_done = 0, buf = 0;
+    Built batch;
+    double sum_n2 = 0, sum_nr = 0, sum_n = 0;
+  } job;
+  int job_buf = 0, dslot_i = 0, pslot_i = 0, preslot_i = 0;
+  bool dec_inflight = false;
+  cudaEvent_t dec_ev = nullptr;
+  std::vector<int> dec_members;
+  int cur_split = D.fixed_split >= -1 ? D.fixed_split : -1;
+  int last_dec_split = -3, last_pf_split = -3;
+  cudaEvent_t last_pf_ev = nullptr;
+  bool decode_seen = false;
+  int split_changes = 0, handoffs = 0, iters = 0, groups = 0;
+  int64_t pf_tokens = 0, dc_tokens = 0;
+
+  auto streams = [&](int sp, cudaStream_t* ds, cudaStream_t* ps, int* dsms, int* psms) {
+    mux_stream_t a, b;
+    int r2 = mux_partition_query(e->part, sp, dsms, psms, &a, &b);
+    *ds = reinterpret_cast<cudaStream_t>(a);
+    *ps = reinterpret_cast<cudaStream_t>(b);
+    return r2;
+  };
+  auto release = [&](Req& r) {
+    r.finished = true;
+    if (!D.keep_pages && !r.pages.empty()) mux_pool_free_pages(e->pool, static_cast<int32_t>(r.pages.size()), r.pages.data());
+  };
+  auto choose_split = [&]() -> int {
+    if (D.fixed_split >= -1) return D.fixed_split;
+    double sum_r = 0;
+    for (int i : decode) sum_r += e->reqs[i].ctx;
+    int best = -1, best_sms = 1 << 30, big = -1, big_sms = -1;
+    for (int i = 0; i < nsplit; ++i) {
+      int ds, ps;
+      mux_partition_query(e->part, i, &ds, &ps, nullptr, nullptr);
+      const double worst = eq2(&e->dec_theta[3 * i], sum_r, static_cast<int>(decode.size())) * e->slowdown[i] * NT;
+      if (worst <= D.tbt_slo_us && ds < best_sms) {
+        best = i;
+        best_sms = ds;
+      }
+      if (ds > big_sms) {
+        big = i;
+        big_sms = ds;
+      }
+    }
+    return best >= 0 ? best : big;  // infeasible SLO: the largest decode share
+  };
+
+  while (true) {
+    bool did = false;
+    // ---- 1. decode iteration completed: tokens "returned", finished requests retire
+    if (dec_inflight && cudaEventQuery(dec_ev) == cudaSuccess) {
+      dec_inflight = false;
+      did = true;
+      std::vector<int> keep;
+      for (int i : dec_members) {
+        Req& r = e->reqs[i];
+        if (--r.gen_left == 0) release(r);
+        else keep.push_back(i);
+      }
+      decode = keep;
+    }
+    // ---- 2. prefill groups completed (in order); a finished prefill is ready to merge
+    while (!pf_out.empty() && cudaEventQuery(pf_out.front().ev) == cudaSuccess) {
+      Group g = pf_out.front();
+      pf_out.pop_front();
+      did = true;
+      if (g.last)
+        for (int i : g.reqs) {
+          Req& r = e->reqs[i];
+          if (r.gen_left > 0) ready.push_back(i);
+          else release(r);
+        }
+    }
+    // ---- 3. next decode iteration (launched first)
+    if (!dec_inflight) {
+      while (!ready.empty() && static_cast<int>(decode.size()) < D.max_decode_seqs) {
+        decode.push_back(ready.front());
+        ready.erase(ready.begin());
+      }
+      if (!decode.empty()) {
+        decode_seen = true;
+        const int sp = choose_split();
+        if (last_dec_split != -3 && sp != last_dec_split) ++split_changes;
+        cur_split = sp;
+        cudaStream_t ds, ps;
+        int dsms, psms;
+        if ((rc = streams(sp, &ds, &ps, &dsms, &psms))) return rc;
+        std::vector<Req*> rs;
+        std::vector<int> nn, kv, p0;
+        for (int i : decode) {
+          Req& r = e->reqs[i];
+          if (r.ctx % kPage == 0) {  // the new token opens a page
+            int32_t id;
+            if ((rc = mux_pool_alloc_pages(e->pool, 1, &id))) return rc;
+            r.pages.push_back(id);
+          }
+          p0.push_back(r.ctx);
+          r.ctx += 1;
+          rs.push_back(&r);
+          nn.push_back(1);
+          kv.push_back(r.ctx);
+        }
+        Slot& s = e->dslot[dslot_i];
+        dslot_i ^= 1;
+        if ((rc = slot_acquire(s))) return rc;
+        Built bt = build_batch(s, rs, nn, kv, p0, D.src_rows);
+        MUX_CUDA(cudaMemcpyAsync(s.d, s.h, bt.n * 4, cudaMemcpyHostToDevice, ds));
+        MUX_CUDA(cudaEventRecord(s.done, ds));
+        s.used = true;
+        const int B = bt.rows;
+        if ((rc = gather(D.src_q, e->dq, bt.d_idx, B, static_cast<int>(qrow), ds))) return rc;
+        if ((rc = gather(D.src_k, e->dk, bt.d_idx, B, static_cast<int>(kvrow), ds))) return rc;
+        if ((rc = gather(D.src_v, e->dv, bt.d_idx, B, static_cast<int>(kvrow), ds))) return rc;
+        mux_side side{};
+        side.batch = &bt.b;
+        side.num_q_heads = Hq;
+        side.q = e->dq;
+        side.k_new = e->dk;
+        side.v_new = e->dv;
+        side.o = e->do_;
+        side.o_dtype = MUX_DTYPE_BF16;
+        side.scale = D.scale;
+        side.layer0 = 0;
+        side.num_layers = NT;
+        side.append = 1;
+        side.num_splits = 0;
+        side.ws = e->ws;
+        side.ws_bytes = e->ws_bytes;
+        if (D.w_o) {
+          side.w_o = D.w_o;
+          side.y = e->dy;
+          side.hidden = D.hidden;
+          side.y_dtype = MUX_DTYPE_BF16;
+        }
+        int li;
+        if ((rc = log_pair(e, &li))) return rc;
+        if ((rc = run_side(e->pool, &side, true, dsms, ds, e->log + li, e->log + li + 1))) return rc;
+        e->iv.push_back({0, li, sp, B});
+        if ((rc = new_event(e, &dec_ev))) return rc;
+        MUX_CUDA(cudaEventRecord(dec_ev, ds));
+        dec_members = decode;
+        dec_inflight = true;
+        last_dec_split = sp;
+        dc_tokens += B;
+        ++iters;
+        did = true;
+      }
+    }
+    // ---- 4. admit the next prefill batch (FCFS, up to max_prefill_tokens new tokens)
+    if (!job.active && !queue.empty()) {
+      job = Job();
+      int tok = 0;
+      while (!queue.empty() && (job.reqs.empty() || tok + e->reqs[queue.front()].r.prompt <= D.max_prefill_tokens)) {
+        tok += e->reqs[queue.front()].r.prompt;
+        job.reqs.push_back(queue.front());
+        queue.pop_front();
+      }
+      job.active = true;
+      job.buf = job_buf;
+      job_buf ^= 1;
+      // target stream of the prep work: that of the first group
+      const int sp = (decode.empty() && ready.empty() && !dec_inflight) ? -1 : cur_split;
+      cudaStream_t ds, ps;
+      int dsms, psms;
+      if ((rc = streams(sp, &ds, &ps, &dsms, &psms))) return rc;
+      if (last_pf_ev && sp != last_pf_split) MUX_CUDA(cudaStreamWaitEvent(ps, last_pf_ev, 0));
+      std::vector<Req*> rs, pre_rs;
+      std::vector<int> nn, kv, p0, pre_n, pre_kv, pre_p0;
+      for (int i : job.reqs) {
+        Req& r = e->reqs[i];
+        const int L = r.r.cached + r.r.prompt;
+        const int np = (L + kPage - 1) / kPage;
+        r.pages.resize(np);
+        if ((rc = mux_pool_alloc_pages(e->pool, np, r.pages.data()))) return rc;
+        rs.push_back(&r);
+        nn.push_back(r.r.prompt);
+        kv.push_back(L);
+        p0.push_back(r.r.cached);
+        if (r.r.cached > 0) {
+          pre_rs.push_back(&r);
+          pre_n.push_back(r.r.cached);
+          pre_kv.push_back(r.r.cached);
+          pre_p0.push_back(0);
+        }
+        r.ctx = L;
+        const double n = r.r.prompt, rr = r.r.cached;
+        job.sum_n2 += n * n;
+        job.sum_nr += n * rr;
+        job.sum_n += n;
+        pf_tokens += r.r.prompt;
+      }
+      // cached prefix: already "in the pool" when the request arrives -> preload every layer
+      if (!pre_rs.empty()) {
+        Slot& s = e->preslot[preslot_i];
+        preslot_i ^= 1;
+        if ((rc = slot_acquire(s))) return rc;
+        Built pb = build_batch(s, pre_rs, pre_n, pre_kv, pre_p0, D.src_rows);
+        MUX_CUDA(cudaMemcpyAsync(s.d, s.h, pb.n * 4, cudaMemcpyHostToDevice, ps));
+        MUX_CUDA(cudaEventRecord(s.done, ps));
+        s.used = true;
+        if ((rc = gather(D.src_k, e->prek, pb.d_idx, pb.rows, static_cast<int>(kvrow), ps))) return rc;
+        if ((rc = gather(D.src_v, e->prev, pb.d_idx, pb.rows, static_cast<int>(kvrow), ps))) return rc;
+        for (int l = 0; l < NT; ++l)
+          if ((rc = mux_append_kv(e->pool, l, &pb.b, e->prek, e->prev, reinterpret_cast<mux_stream_t>(ps)))) return rc;
+      }
+      Slot& s = e->pslot[pslot_i];
+      pslot_i ^= 1;
+      if ((rc = slot_acquire(s))) return rc;
+      job.batch = build_batch(s, rs, nn, kv, p0, D.src_rows);
+      MUX_CUDA(cudaMemcpyAsync(s.d, s.h, job.batch.n * 4, cudaMemcpyHostToDevice, ps));
+      MUX_CUDA(cudaEventRecord(s.done, ps));
+      s.used = true;
+      const int T = job.batch.rows;
+      if ((rc = gather(D.src_q, e->pq[job.buf], job.batch.d_idx, T, static_cast<int>(qrow), ps))) return rc;
+      if ((rc = gather(D.src_k, e->pk[job.buf], job.batch.d_idx, T, static_cast<int>(kvrow), ps))) return rc;
+      if ((rc = gather(D.src_v, e->pv[job.buf], job.batch.d_idx, T, static_cast<int>(kvrow), ps))) return rc;
+      cudaEvent_t prep;
+      if ((rc = new_event(e, &prep))) return rc;
+      MUX_CUDA(cudaEventRecord(prep, ps));
+      last_pf_ev = prep;
+      last_pf_split = sp;
+      did = true;
+    }
+    // ---- 5. keep up to two prefill groups of N_PL layers queued (layer-wise prefill)
+    if (job.active && job.layers_done < NT && pf_out.size() < 2) {
+      const bool dec_idle = decode.empty() && ready.empty() && !dec_inflight;
+      int sp = cur_split;
+      if (dec_idle && (D.handoff || !decode_seen)) {
+        if (sp != -1 && decode_seen && last_pf_split != -1) ++handoffs;
+        sp = -1;  // no decode work: every SM to the prefill (P:531 hand-off)
+      }
+      cudaStream_t ds, ps;
+      int dsms, psms;
+      if ((rc = streams(sp, &ds, &ps, &dsms, &psms))) return rc;
+      if (last_pf_ev && sp != last_pf_split) MUX_CUDA(cudaStreamWaitEvent(ps, last_pf_ev, 0));
+      int npl = NT;
+      if (D.fixed_pl > 0) {
+        npl = D.fixed_pl;
+      } else if (!e->dec_theta.empty() && !dec_idle && sp >= 0) {
+        double sum_r = 0;
+        for (int i : decode) sum_r += e->reqs[i].ctx;
+        const double td = eq2(&e->dec_theta[3 * sp], sum_r, static_cast<int>(decode.size()));
+        const double tp = eq1(&e->pf_theta[4 * sp], job.sum_n2, job.sum_nr, job.sum_n);
+        // N_PL = ceil(T_d N_T / T_P) with T_d = N_T td, T_P = N_T tp (per-layer predictions)
+        npl = mux_num_prefill_layers(td * NT, tp * NT, NT, NT - job.layers_done);
+      }
+      npl = std::max(1, std::min(npl, NT - job.layers_done));
+      mux_side side{};
+      side.batch = &job.batch.b;
+      side.num_q_heads = Hq;
+      side.q = e->pq[job.buf];
+      side.k_new = e->pk[job.buf];
+      side.v_new = e->pv[job.buf];
+      side.o = e->po[job.buf];
+      side.o_dtype = MUX_DTYPE_BF16;
+      side.scale = D.scale;
+      side.layer0 = job.layers_done;
+      side.num_layers = npl;
+      side.append = 1;
+      if (D.w_o) {
+        side.w_o = D.w_o;
+        side.y = e->py[job.buf];
+        side.hidden = D.hidden;
+        side.y_dtype = MUX_DTYPE_BF16;
+      }
+      int li;
+      if ((rc = log_pair(e, &li))) return rc;
+      if ((rc = run_side(e->pool, &side, false, psms, ps, e->log + li, e->log + li + 1))) return rc;
+      e->iv.push_back({1, li, sp, job.batch.rows});
+      Group g;
+      if ((rc = new_event(e, &g.ev))) return rc;
+      MUX_CUDA(cudaEventRecord(g.ev, ps));
+      job.layers_done += npl;
+      g.last = job.layers_done == NT;
+      if (g.last) {
+        g.reqs = job.reqs;
+        for (int i : job.reqs) e->reqs[i].ttft_log = li + 1;
+        job.active = false;
+      }
+      pf_out.push_back(g);
+      last_pf_ev = g.ev;
+      last_pf_split = sp;
+      ++groups;
+      did = true;
+    }
+    // ---- 6. done?
+    if (!dec_inflight && pf_out.empty() && !job.active && queue.empty() && ready.empty() && decode.empty()) break;
+    if (!did) std::this_thread::yield();
+  }
+  MUX_CUDA(cudaDeviceSynchronize());
+
+  // ---- statistics from the device log
+  std::vector<unsigned long long> lg(e->log_n);
+  if (e->log_n) MUX_CUDA(cudaMemcpy(lg.data(), e->log, e->log_n * 8, cudaMemcpyDeviceToHost));
+  mux_engine_stats S{};
+  unsigned long long t_first = ~0ull, t_last = 0;
+  for (auto& v : e->iv) {
+    t_first = std::min(t_first, lg[v.log]);
+    t_last = std::max(t_last, lg[v.log + 1]);
+  }
+  double bub[2] = {0, 0}, busy[2] = {0, 0};
+  int have[2] = {0, 0};
+  for (int side = 0; side < 2; ++side) {
+    std::vector<std::pair<unsigned long long, unsigned long long>> xs;
+    for (auto& v : e->iv)
+      if (v.side == side) xs.push_back({lg[v.log], lg[v.log + 1]});
+    if (xs.empty()) continue;
+    std::sort(xs.begin(), xs.end());
+    unsigned long long w0 = xs.front().first, w1 = 0, cs = xs.front().first, ce = xs.front().second;
+    double b = 0;
+    for (auto& x : xs) {
+      w1 = std::max(w1, x.second);
+      if (x.first > ce) {
+        b += static_cast<double>(ce - cs);
+        cs = x.first;
+        ce = x.second;
+      } else {
+        ce = std::max(ce, x.second);
+      }
+    }
+    b += static_cast<double>(ce - cs);
+    busy[side] = b * 1e-3;
+    bub[side] = w1 > w0 ? 1.0 - b / static_cast<double>(w1 - w0) : 0.0;
+    have[side] = 1;
+  }
+  S.makespan_us = t_last > t_first ? (t_last - t_first) * 1e-3 : 0.0;
+  S.prefill_tokens = pf_tokens;
+  S.decode_tokens = dc_tokens;
+  S.decode_iters = iters;
+  S.prefill_groups = groups;
+  S.split_changes = split_changes;
+  S.handoffs = handoffs;
+  S.busy_dec_us = busy[0];
+  S.busy_pf_us = busy[1];
+  S.bubble_ratio_dec = bub[0];
+  S.bubble_ratio_pf = bub[1];
+  S.bubble_ratio = (have[0] + have[1]) ? (bub[0] * have[0] + bub[1] * have[1]) / (have[0] + have[1]) : 0.0;
+  unsigned long long prev_end = 0;
+  double tsum = 0;
+  int tn = 0;
+  for (auto& v : e->iv) {
+    if (v.side != 0) continue;
+    if (prev_end) {
+      const double t = (lg[v.log + 1] - prev_end) * 1e-3;
+      tsum += t;
+      ++tn;
+      S.tbt_max_us = std::max(S.tbt_max_us, t);
+    }
+    prev_end = lg[v.log + 1];
+  }
+  S.tbt_mean_us = tn ? tsum / tn : 0.0;
+  double fsum = 0;
+  int fn = 0;
+  for (auto& r : e->reqs)
+    if (r.ttft_log >= 0) {
+      const double t = (lg[r.ttft_log] - t_first) * 1e-3;
+      fsum += t;
+      ++fn;
+      S.ttft_max_us = std::max(S.ttft_max_us, t);
+    }
+  S.ttft_mean_us = fn ? fsum / fn : 0.0;
+  if (st) *st = S;
+  return MUX_OK;
+}
+
+int mux_engine_request_pages(mux_engine_t e, int32_t id, int32_t* kv_len, int32_t* page_ids, int32_t cap,
+                             int32_t* n_pages) {
+  if (!e) return fail(MUX_ERR_INVALID_ARG, "engine NULL");
+  for (auto& r : e->reqs)
+    if (r.r.id == id) {
+      if (kv_len) *kv_len = r.ctx;
+      const int n = static_cast<int>(r.pages.size());
+      if (n_pages) *n_pages = n;
+      if (page_ids)
+        for (int i = 0; i < n && i < cap; ++i) page_ids[i] = r.pages[i];
+      return MUX_OK;
+    }
+  return fail(MUX_ERR_INVALID_ARG, "no request with this id");
+}
+
+int mux_engine_trace(mux_engine_t e, int64_t* out, int32_t cap, int32_t* n) {
+  if (!e || !n) return fail(MUX_ERR_INVALID_ARG, "bad argument");
+  std::vector<unsigned long long> lg(e->log_n);
+  if (e->log_n) MUX_CUDA(cudaMemcpy(lg.data(), e->log, e->log_n * 8, cudaMemcpyDeviceToHost));
+  int k = 0;
+  for (auto& v : e->iv) {
+    if (out && k < cap) {
+      out[6 * k + 0] = v.side;
+      out[6 * k + 1] = v.split;
+      out[6 * k + 2] = v.batch;
+      out[6 * k + 3] = static_cast<int64_t>(lg[v.log]);
+      out[6 * k + 4] = static_cast<int64_t>(lg[v.log + 1]);
+      out[6 * k + 5] = 0;
+    }
+    ++k;
+  }
+  *n = k;
+  return MUX_OK;
+}
+
+int mux_engine_destroy(mux_engine_t e) {
+  if (!e) return MUX_OK;
+  cudaDeviceSynchronize();
+  for (void* p : {e->dq, e->dk, e->dv, e->do_, e->dy, e->ws, e->prek, e->prev})
+    if (p) cudaFree(p);
+  for (int i = 0; i < 2; ++i) {
+    for (void* p : {e->pq[i], e->pk[i], e->pv[i], e->po[i], e->py[i]})
+      if (p) cudaFree(p);
+    for (Slot* s : {&e->dslot[i], &e->pslot[i], &e->preslot[i]}) {
+      if (s->h) cudaFreeHost(s->h);
+      if (s->d) cudaFree(s->d);
+      if (s->done) cudaEventDestroy(s->done);
+    }
+  }
+  if (e->log) cudaFree(e->log);
+  for (auto ev : e->events) cudaEventDestroy(ev);
+  delete e;
+  return MUX_OK;
+}
+
+}  // extern "C"

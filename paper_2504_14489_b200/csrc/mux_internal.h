@@ -63,6 +63,12 @@ struct PoolImpl;  // pool.cu
 // validated view of a batch (host side)
 int validate_batch(const mux_batch* b, bool need_decode_shape);
 
+// partition.cu: enqueue one side's layers (append + attention (+ combine) + out-projection +
+// hook per layer) on `st`; t0/t1: optional %globaltimer stamps before / after
+int run_side(mux_pool_t pool, const mux_side* s, bool decode, int sms, cudaStream_t st, unsigned long long* t0,
+             unsigned long long* t1);
+void launch_stamp(unsigned long long* dst, cudaStream_t st);
+
 }  // namespace mux
 
 // ============================================================================ device side

@@ -160,8 +160,13 @@ int mux_partition_memory(mux_part_t p, int64_t* bytes) {
   return MUX_OK;
 }
 
-static int run_side(mux_pool_t pool, const mux_side* s, bool decode, int sms, cudaStream_t st,
-                    unsigned long long* t0, unsigned long long* t1) {
+}  // extern "C"
+
+namespace mux {
+void launch_stamp(unsigned long long* dst, cudaStream_t st) { stamp_kernel<<<1, 1, 0, st>>>(dst); }
+
+int run_side(mux_pool_t pool, const mux_side* s, bool decode, int sms, cudaStream_t st, unsigned long long* t0,
+             unsigned long long* t1) {
   if (s->w_o && (s->o_dtype != MUX_DTYPE_BF16 || !s->y || s->hidden < 1))
     return fail(MUX_ERR_INVALID_ARG, "out-projection needs bf16 o, y and hidden >= 1");
   if (t0) stamp_kernel<<<1, 1, 0, st>>>(t0);
@@ -204,6 +209,9 @@ static int run_side(mux_pool_t pool, const mux_side* s, bool decode, int sms, cu
   MUX_CUDA(cudaGetLastError());
   return MUX_OK;
 }
+}  // namespace mux
+
+extern "C" {
 
 int mux_run_layer(mux_part_t part, int32_t split_idx, mux_pool_t pool, const mux_side* prefill,
                   const mux_side* decode, mux_side_times* times, mux_stream_t join_stream) {
