@@ -309,6 +309,8 @@ typedef struct {
   int32_t fixed_pl;             /* > 0: layers per prefill group instead of N_PL */
   int32_t handoff;              /* 1: decode termination hands the prefill to the whole GPU */
   int32_t keep_pages;           /* 1: finished requests keep their pages (for inspection) */
+  int32_t serialize;            /* 1: temporal multiplexing baseline: both sides on ONE whole-GPU
+                                   stream (no overlap); fixed_split must be -1 */
 } mux_engine_desc;
 
 typedef struct {

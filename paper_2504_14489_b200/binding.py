@@ -59,7 +59,7 @@ class EngineDesc(ctypes.Structure):
                 ("src_rows", c_i32), ("w_o", c_p), ("hidden", c_i32), ("max_decode_seqs", c_i32),
                 ("max_prefill_tokens", c_i32), ("fixed_split", c_i32), ("n_cost", c_i32), ("dec_theta", c_p),
                 ("pf_theta", c_p), ("dec_slowdown", c_p), ("tbt_slo_us", c_dbl), ("fixed_pl", c_i32),
-                ("handoff", c_i32), ("keep_pages", c_i32)]
+                ("handoff", c_i32), ("keep_pages", c_i32), ("serialize", c_i32)]
 
 
 class RequestC(ctypes.Structure):
@@ -463,7 +463,7 @@ class Engine:
     def __init__(self, part: "Partition", pool: Pool, num_q_heads: int, src_q, src_k, src_v, *,
                  scale: float, w_o: "PackedW" = None, max_decode_seqs: int = 256,
                  max_prefill_tokens: int = 16384, fixed_split: int = -2, cost=None, tbt_slo_us: float = 1e30,
-                 fixed_pl: int = 0, handoff: bool = True, keep_pages: bool = False):
+                 fixed_pl: int = 0, handoff: bool = True, keep_pages: bool = False, serialize: bool = False):
         d = EngineDesc()
         d.num_q_heads, d.scale = num_q_heads, scale
         d.src_q, d.src_k, d.src_v = _ptr(src_q), _ptr(src_k), _ptr(src_v)
@@ -472,7 +472,7 @@ class Engine:
             d.w_o, d.hidden = _ptr(w_o.data), int(w_o.N)
         d.max_decode_seqs, d.max_prefill_tokens = max_decode_seqs, max_prefill_tokens
         d.fixed_split, d.tbt_slo_us, d.fixed_pl = fixed_split, tbt_slo_us, fixed_pl
-        d.handoff, d.keep_pages = int(handoff), int(keep_pages)
+        d.handoff, d.keep_pages, d.serialize = int(handoff), int(keep_pages), int(serialize)
         self._keep = [src_q, src_k, src_v, w_o]
         if cost is not None:
             n = part.n

@@ -108,4 +108,5 @@ class CostModel:
     @staticmethod
     def load(path: str) -> "CostModel":
         with open(path) as f:
-            return CostModel.from_json(json.load(f))
+            d = json.load(f)
+        return CostModel.from_json(d["model"] if "model" in d else d)  # profile_costmodel.py output or bare

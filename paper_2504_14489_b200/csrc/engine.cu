@@ -159,6 +159,7 @@ int mux_engine_create(mux_engine_t* out, mux_part_t part, mux_pool_t pool, const
   const int nsplit = mux_partition_count(part);
   if (desc->fixed_split < -2 || desc->fixed_split >= nsplit) return fail(MUX_ERR_INVALID_ARG, "fixed_split out of range");
   const bool model = desc->dec_theta && desc->pf_theta;
+  if (desc->serialize && desc->fixed_split != -1) return fail(MUX_ERR_INVALID_ARG, "serialize needs fixed_split = -1");
   if (desc->fixed_split == -2 && (!model || desc->n_cost != nsplit))
     return fail(MUX_ERR_INVALID_ARG, "best-fit split needs a cost model with one entry per split");
   auto* e = new mux_engine();
@@ -322,7 +323,7 @@ int mux_engine_run(mux_engine_t e, mux_engine_stats* st) {
     mux_stream_t a, b;
     int r2 = mux_partition_query(e->part, sp, dsms, psms, &a, &b);
     *ds = reinterpret_cast<cudaStream_t>(a);
-    *ps = reinterpret_cast<cudaStream_t>(b);
+    *ps = D.serialize ? *ds : reinterpret_cast<cudaStream_t>(b);  // one stream: no overlap
     return r2;
   };
   auto release = [&](Req& r) {
@@ -384,7 +385,9 @@ int mux_engine_run(mux_engine_t e, mux_engine_stats* st) {
       }
       if (!decode.empty()) {
         decode_seen = true;
-        const int sp = choose_split();
+        // no prefill work left anywhere: the decode iterations get the whole GPU (R24)
+        const bool pf_idle = !job.active && queue.empty() && pf_out.empty();
+        const int sp = pf_idle ? -1 : choose_split();
         if (last_dec_split != -3 && sp != last_dec_split) ++split_changes;
         cur_split = sp;
         cudaStream_t ds, ps;

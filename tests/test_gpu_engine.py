@@ -128,14 +128,17 @@ def test_engine_best_fit_and_npl(mux, part):
     _check_stats(s)
     tr = eng.trace()
     dec_splits = set(tr[tr[:, 0] == 0, 1].tolist())
-    assert dec_splits == {1}, dec_splits
+    # split 1 while a prefill runs, the whole GPU (-1) once no prefill work is left (R24)
+    assert 1 in dec_splits and dec_splits <= {1, -1}, dec_splits
     _check_pool(eng, pool, src)
     eng.close()
 
 
-def test_engine_time_sliced_full_gpu(mux, part):
-    """fixed_split = -1: both sides on whole-GPU streams (the non-partitioned baseline)."""
-    eng, pool, s, src = _run(mux, part, fixed_split=-1)
+@pytest.mark.parametrize("serialize", [False, True])
+def test_engine_unpartitioned_and_time_sliced(mux, part, serialize):
+    """fixed_split = -1: both sides on whole-GPU streams (unpartitioned), or on one stream
+    (serialize: the temporal-multiplexing baseline)."""
+    eng, pool, s, src = _run(mux, part, fixed_split=-1, serialize=serialize)
     _check_stats(s)
     _check_pool(eng, pool, src)
     eng.close()
