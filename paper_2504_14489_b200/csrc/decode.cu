@@ -449,7 +449,10 @@ int32_t mux_decode_num_splits(int32_t num_seqs, int32_t hkv, int32_t head_dim, c
           q.push(st + t);
           span = std::max(span, st + t);
         }
-    span = std::max(span, hbm_floor_us);  // the chip's HBM bandwidth caps any SM count
+    // the chip's HBM bandwidth caps any SM count; near the cap the SMs' streams interfere, so
+    // the smaller of the two terms still counts a quarter (fitted to the cfg2 decode on 148 SMs:
+    // 2 splits 168 us vs 1 split 178 us measured)
+    span = std::max(span, hbm_floor_us) + 0.25 * std::min(span, hbm_floor_us);
     if (S > 1) span += 6.0 + static_cast<double>(num_seqs) * hkv * 8 * S * (head_dim + 2) * 4 / (num_sms * 1.0e5);
     if (span < best_t * 0.98) {  // a finer split must win by > 2% (model noise)
       best_t = span;
