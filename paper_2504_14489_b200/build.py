@@ -15,6 +15,8 @@ NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",
          "--expt-relaxed-constexpr", "-Xcompiler", "-fPIC,-fvisibility=hidden", "-Xptxas", "-v",
          "-I", os.path.join(ROOT, "include")]
+# developer A/B builds only (e.g. MUX_NVCC_EXTRA="-DMUX_EMU_PAIRS=0x1111u"); empty in production
+FLAGS += os.environ.get("MUX_NVCC_EXTRA", "").split()
 
 
 def sources():
