@@ -68,6 +68,9 @@ int validate_batch(const mux_batch* b, bool need_decode_shape);
 int run_side(mux_pool_t pool, const mux_side* s, bool decode, int sms, cudaStream_t st, unsigned long long* t0,
              unsigned long long* t1);
 void launch_stamp(unsigned long long* dst, cudaStream_t st);
+// outproj.cu: mux_outproj with the SM count of the launching partition (persistent grid)
+int outproj_launch(const void* x, const void* w, void* y, int32_t y_dtype, int32_t T, int32_t K, int32_t N,
+                   mux_stream_t stream, int num_sms);
 
 }  // namespace mux
 

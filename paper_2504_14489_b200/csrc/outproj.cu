@@ -13,10 +13,12 @@
 // load of the row-major W fetched 128-byte rows 8 KiB apart and capped the skinny kernel at
 // ~40 GB/s per SM (ncu, profiles/r01_summary.md).
 //
-// Tile kernel (T > 128): one CTA per 128 x 256 output tile, 6 warps: warp 4 = producer (TMA for
-// X, bulk copies for W), warp 5 = TMEM owner + single-thread tcgen05.mma issuer, warps 0-3 =
-// epilogue (thread = output row).  4-stage ring of {A: X 128 rows x 64 k (K-major, TMA
-// SWIZZLE_128B), B: 2 packed W tiles = 64 k x 256 n (MN-major)}, 48 KiB per stage.
+// Tile kernel (T > 128): persistent, one CTA per SM of the side's partition walking 128 x 256
+// output tiles, 6 warps: warp 4 = producer (TMA for X, bulk copies for W), warp 5 = TMEM owner
+// + single-thread tcgen05.mma issuer, warps 0-3 = epilogue (thread = output row).  4-stage ring
+// of {A: X 128 rows x 64 k (K-major, TMA SWIZZLE_128B), B: 2 packed W tiles = 64 k x 256 n
+// (MN-major)}, 48 KiB per stage; two 256-column TMEM accumulators so a tile's epilogue
+// overlaps the next tile's mainloop.
 //
 // Skinny kernel (T <= 128, the decode side: one token per sequence): the 128-row M tile would
 // be mostly zero fill, so it computes the transpose Y^T = W^T . X^T: M = 128 columns of W (A =
@@ -26,6 +28,8 @@
 // ~100 GB/s of smem fill per SM (bytes in flight / DRAM latency), so on a decode partition its
 // time is W + X-re-read bytes / (SMs x ~100 GB/s).
 // Rows / columns past T / N come from TMA zero fill or packing pads and are not stored.
+#include <algorithm>
+
 #include "pool.h"
 
 namespace mux {
@@ -40,7 +44,8 @@ struct GemmSmem {
   static constexpr int kB = kGBK * kGBN * 2;          // 32 KiB
   static constexpr int kStage = kA + kB;
   static constexpr int kBar = kGStages * kStage;
-  static constexpr int kTmemSlot = kBar + (2 * kGStages + 1) * 8;
+  // full[4] empty[4] acc_full[2] acc_empty[2]
+  static constexpr int kTmemSlot = kBar + (2 * kGStages + 4) * 8;
   static constexpr int kBytes = kTmemSlot + 16;
 };
 
@@ -48,6 +53,7 @@ struct GemmParams {
   void* y;
   const uint8_t* w_pk;
   int T, N, K, y_f32;
+  int m_tiles, n_tiles;
 };
 
 __device__ __forceinline__ void store_row32(const GemmParams& p, int row, int col, const uint32_t* v) {
@@ -79,6 +85,9 @@ __device__ __forceinline__ void store_row32(const GemmParams& p, int row, int co
   }
 }
 
+// Persistent: CTA c walks tiles c, c + gridDim.x, ... (n fastest: co-running CTAs share a few
+// X row panels while all of the packed W stays in L2).  The smem ring runs continuously across tiles, and the accumulator
+// is double-buffered in TMEM (2 x 256 columns): tile i+1's mainloop overlaps tile i's epilogue.
 __global__ void __launch_bounds__(kGThreads, 1)
     outproj_kernel(const __grid_constant__ CUtensorMap tmap_x, const GemmParams p) {
   using L = GemmSmem;
@@ -87,19 +96,20 @@ __global__ void __launch_bounds__(kGThreads, 1)
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + L::kBar);
   uint64_t* empty = full + kGStages;
   uint64_t* acc_full = empty + kGStages;
+  uint64_t* acc_empty = acc_full + 2;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem + L::kTmemSlot);
   const int warp = dev::warp_idx_uniform(), lane = threadIdx.x & 31;
-  const int m0 = blockIdx.y * kGBM, n0 = blockIdx.x * kGBN;
   const int nk = (p.K + kGBK - 1) / kGBK;
-  const int ntiles = (p.N + 127) / 128;
-  const int nt0 = blockIdx.x * 2;
-  const bool second = nt0 + 1 < ntiles;  // N tail: the second 128-column tile may not exist
+  const int ntiles = (p.N + 127) / 128;                       // 128-column packed W tiles
+  const int tiles = p.m_tiles * p.n_tiles;
 
   if (threadIdx.x == 0) {
-    for (int i = 0; i < 2 * kGStages + 1; ++i) dev::mbar_init(&full[i], 1);
+    for (int i = 0; i < 2 * kGStages + 2; ++i) dev::mbar_init(&full[i], 1);
+    dev::mbar_init(&acc_empty[0], 4);
+    dev::mbar_init(&acc_empty[1], 4);
     dev::fence_mbar_init();
   }
-  if (warp == 5) dev::tmem_alloc(tmem_slot, 256);
+  if (warp == 5) dev::tmem_alloc(tmem_slot, 512);
   dev::tc_fence_before();
   __syncthreads();
   dev::tc_fence_after();
@@ -108,17 +118,22 @@ __global__ void __launch_bounds__(kGThreads, 1)
   if (warp == 4) {
     if (lane == 0) {
       dev::tma_prefetch(&tmap_x);
-      const uint8_t* w0 = p.w_pk + static_cast<size_t>(nt0) * nk * kPackTile;
-      const uint8_t* w1 = w0 + static_cast<size_t>(nk) * kPackTile;
-      for (int kb = 0; kb < nk; ++kb) {
-        const int s = kb % kGStages;
-        if (kb >= kGStages) dev::mbar_wait_sleep(&empty[s], ((kb / kGStages) - 1) & 1);
-        dev::mbar_expect_tx(&full[s], L::kA + (second ? 2 : 1) * kPackTile);
-        uint8_t* a = smem + s * L::kStage;
-        uint8_t* bt = a + L::kA;
-        dev::tma_load_3d(a, &tmap_x, &full[s], kb * kGBK, m0, 0);
-        dev::bulk_load(bt, w0 + static_cast<size_t>(kb) * kPackTile, kPackTile, &full[s]);
-        if (second) dev::bulk_load(bt + kPackTile, w1 + static_cast<size_t>(kb) * kPackTile, kPackTile, &full[s]);
+      int it = 0;  // global k-block counter (ring position)
+      for (int t = blockIdx.x; t < tiles; t += gridDim.x) {
+        const int m0 = (t / p.n_tiles) * kGBM, nt0 = (t % p.n_tiles) * 2;
+        const bool second = nt0 + 1 < ntiles;
+        const uint8_t* w0 = p.w_pk + static_cast<size_t>(nt0) * nk * kPackTile;
+        const uint8_t* w1 = w0 + static_cast<size_t>(nk) * kPackTile;
+        for (int kb = 0; kb < nk; ++kb, ++it) {
+          const int s = it % kGStages;
+          if (it >= kGStages) dev::mbar_wait_sleep(&empty[s], ((it / kGStages) - 1) & 1);
+          dev::mbar_expect_tx(&full[s], L::kA + (second ? 2 : 1) * kPackTile);
+          uint8_t* a = smem + s * L::kStage;
+          uint8_t* bt = a + L::kA;
+          dev::tma_load_3d(a, &tmap_x, &full[s], kb * kGBK, m0, 0);
+          dev::bulk_load(bt, w0 + static_cast<size_t>(kb) * kPackTile, kPackTile, &full[s]);
+          if (second) dev::bulk_load(bt + kPackTile, w1 + static_cast<size_t>(kb) * kPackTile, kPackTile, &full[s]);
+        }
       }
     }
   } else if (warp == 5) {
@@ -126,39 +141,56 @@ __global__ void __launch_bounds__(kGThreads, 1)
       constexpr uint32_t idesc = dev::umma_idesc_bf16(kGBM, kGBN, 0, 1);
       const uint64_t d0 = dev::umma_desc_sw128(dev::smem_u32(smem), 16, 1024);                      // A K-major
       const uint64_t e0 = dev::umma_desc_sw128(dev::smem_u32(smem + L::kA), kGBK * 128, 1024);     // B MN-major
-      for (int kb = 0; kb < nk; ++kb) {
-        const int s = kb % kGStages;
-        dev::mbar_wait_sleep(&full[s], (kb / kGStages) & 1);
+      int it = 0, i = 0;
+      for (int t = blockIdx.x; t < tiles; t += gridDim.x, ++i) {
+        const int b = i & 1;
+        if (i >= 2) dev::mbar_wait_sleep(&acc_empty[b], ((i >> 1) - 1) & 1);   // epilogue drained buffer b
         dev::tc_fence_after();
+        const uint32_t acc = tmem + b * kGBN;
+        for (int kb = 0; kb < nk; ++kb, ++it) {
+          const int s = it % kGStages;
+          dev::mbar_wait_sleep(&full[s], (it / kGStages) & 1);
+          dev::tc_fence_after();
 #pragma unroll
-        for (int kk = 0; kk < kGBK / 16; ++kk)
-          dev::umma_ss(tmem, d0 + ((s * L::kStage + kk * 32) >> 4), e0 + ((s * L::kStage + kk * 16 * 128) >> 4), idesc,
-                       (kb > 0 || kk > 0) ? 1u : 0u);
-        dev::umma_commit(&empty[s]);
+          for (int kk = 0; kk < kGBK / 16; ++kk)
+            dev::umma_ss(acc, d0 + ((s * L::kStage + kk * 32) >> 4), e0 + ((s * L::kStage + kk * 16 * 128) >> 4),
+                         idesc, (kb > 0 || kk > 0) ? 1u : 0u);
+          dev::umma_commit(&empty[s]);
+        }
+        dev::umma_commit(&acc_full[b]);
       }
-      dev::umma_commit(acc_full);
     }
     __syncwarp();
   } else {
-    // epilogue: thread = output row m0 + 32*warp + lane; 256 fp32 columns from TMEM
-    dev::mbar_wait_sleep(acc_full, 0);
-    dev::tc_fence_after();
-    const int row = m0 + warp * 32 + lane;
-    const uint32_t taddr = tmem + (static_cast<uint32_t>(warp * 32) << 16);
-    const int ncols = second ? kGBN : 128;
+    // epilogue: thread = output row m0 + 32*warp + lane; 256 fp32 columns from TMEM buffer b
+    int i = 0;
+    for (int t = blockIdx.x; t < tiles; t += gridDim.x, ++i) {
+      const int b = i & 1;
+      const int m0 = (t / p.n_tiles) * kGBM, nt0 = (t % p.n_tiles) * 2;
+      const int ncols = nt0 + 1 < ntiles ? kGBN : 128;
+      dev::mbar_wait_sleep(&acc_full[b], (i >> 1) & 1);
+      dev::tc_fence_after();
+      const int row = m0 + warp * 32 + lane;
+      const uint32_t taddr = tmem + b * kGBN + (static_cast<uint32_t>(warp * 32) << 16);
 #pragma unroll 1
-    for (int c = 0; c < ncols / 32; ++c) {
-      uint32_t v[32];
-      dev::tmem_ld32(taddr + c * 32, v);
-      dev::tmem_wait_ld();
-      store_row32(p, row, n0 + c * 32, v);
+      for (int c = 0; c < ncols / 32; ++c) {
+        uint32_t v[32];
+        dev::tmem_ld32(taddr + c * 32, v);
+        dev::tmem_wait_ld();
+        if (c == ncols / 32 - 1) {  // every TMEM read of buffer b is done: release it
+          dev::tc_fence_before();
+          __syncwarp();
+          if (lane == 0) dev::mbar_arrive(&acc_empty[b]);
+        }
+        store_row32(p, row, nt0 * 128 + c * 32, v);
+      }
     }
   }
   dev::tc_fence_before();
   __syncthreads();
   if (warp == 5) {
     dev::tc_fence_after();
-    dev::tmem_dealloc(tmem, 256);
+    dev::tmem_dealloc(tmem, 512);
   }
 }
 
@@ -319,8 +351,10 @@ extern "C" int mux_outproj_pack_w(const void* w, void* w_packed, int32_t K, int3
   return MUX_OK;
 }
 
-extern "C" int mux_outproj(const void* x, const void* w, void* y, int32_t y_dtype, int32_t T, int32_t K, int32_t N,
-                           mux_stream_t stream) {
+namespace mux {
+// num_sms: SMs the launch may occupy (the side's partition); <= 0 = the whole device
+int outproj_launch(const void* x, const void* w, void* y, int32_t y_dtype, int32_t T, int32_t K, int32_t N,
+                   mux_stream_t stream, int num_sms) {
   if (!x || !w || !y) return fail(MUX_ERR_INVALID_ARG, "mux_outproj: NULL pointer");
   if (T < 1 || K < 1 || N < 1) return fail(MUX_ERR_INVALID_ARG, "mux_outproj: T, K, N must be >= 1");
   if (y_dtype != MUX_DTYPE_BF16 && y_dtype != MUX_DTYPE_F32) return fail(MUX_ERR_INVALID_ARG, "bad y_dtype");
@@ -362,9 +396,16 @@ extern "C" int mux_outproj(const void* x, const void* w, void* y, int32_t y_dtyp
     MUX_CUDA(cudaFuncSetAttribute(outproj_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
     attr_done = true;
   }
-  GemmParams prm{y, wp, T, N, K, y_dtype == MUX_DTYPE_F32};
-  dim3 grid((N + kGBN - 1) / kGBN, (T + kGBM - 1) / kGBM);
-  outproj_kernel<<<grid, kGThreads, smem, st>>>(tx, prm);
+  GemmParams prm{y, wp, T, N, K, y_dtype == MUX_DTYPE_F32, (T + kGBM - 1) / kGBM, (N + kGBN - 1) / kGBN};
+  const int tiles = prm.m_tiles * prm.n_tiles;
+  const int sms = num_sms > 0 ? num_sms : device_sm_count();
+  outproj_kernel<<<std::min(tiles, std::max(sms, 1)), kGThreads, smem, st>>>(tx, prm);
   MUX_CUDA(cudaGetLastError());
   return MUX_OK;
+}
+}  // namespace mux
+
+extern "C" int mux_outproj(const void* x, const void* w, void* y, int32_t y_dtype, int32_t T, int32_t K, int32_t N,
+                           mux_stream_t stream) {
+  return mux::outproj_launch(x, w, y, y_dtype, T, K, N, stream, 0);
 }

@@ -198,9 +198,9 @@ int run_side(mux_pool_t pool, const mux_side* s, bool decode, int sms, cudaStrea
                             s->scale, reinterpret_cast<mux_stream_t>(st));
     if (rc) return rc;
     if (s->w_o) {
-      rc = mux_outproj(o, at(s->w_o, s->w_stride), const_cast<void*>(at(s->y, s->y_stride)), s->y_dtype,
-                       s->batch->total_q, s->num_q_heads * pool->desc.head_dim, s->hidden,
-                       reinterpret_cast<mux_stream_t>(st));
+      rc = outproj_launch(o, at(s->w_o, s->w_stride), const_cast<void*>(at(s->y, s->y_stride)), s->y_dtype,
+                          s->batch->total_q, s->num_q_heads * pool->desc.head_dim, s->hidden,
+                          reinterpret_cast<mux_stream_t>(st), sms);
       if (rc) return rc;
     }
     if (s->hook) s->hook(s->hook_user, decode ? 0 : 1, i, reinterpret_cast<mux_stream_t>(st));
