@@ -313,6 +313,7 @@ def main():
     ap.add_argument("--layers", type=int, default=0, help="pool layers (default: the model's N_T)")
     ap.add_argument("--split", type=int, default=-2, help="split index; -2 = sweep and pick the best")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--granularity", type=int, default=8, help="decode SM step of the split sweep")
     args = ap.parse_args()
     args.warmup = max(3, args.warmup)
 
@@ -348,7 +349,9 @@ def main():
         assert all(int(x) == wl.page_hash for x in hs), "page tables differ across ranks"
 
     total_sms = mux.mux_device_sm_count(local)
-    configs = mux.mux_partition_configs(total_sms, 16, 12)
+    # decode SM counts in steps of --granularity (the paper's 16 on A100/H100, set by
+    # its cluster kernels; these kernels use no clusters, and green contexts split in 8s)
+    configs = mux.mux_partition_configs(total_sms, args.granularity, 12)
     part = mux.Partition(local, configs)
     # ---- calibration (untimed): isolated side times per split, N_PL balance, predicted mux rate
     sweep = []
