@@ -203,6 +203,11 @@ class Workload:
                            num_splits=ns, ws=self.ws, w_o=self.w_o, y=self.dc_y, hook=self.hooks.get(0))
         return pf, dc, ns
 
+    def set_allreduce_hooks(self, comms):
+        """Per-layer all-reduce of this buffer set's y on each side's own stream (a7, R23)."""
+        self.hooks = {0: lambda side, layer, stream: comms[0].all_reduce_(self.dc_y, stream),
+                      1: lambda side, layer, stream: comms[1].all_reduce_(self.pf_y, stream)}
+
     def outproj_flops_layer(self, side):
         return 2.0 * side.total_new * self.Hq * self.d * self.hidden
 
@@ -340,8 +345,7 @@ def main():
         # the side's own (green-context) stream from the mux_run_layer hook
         from paper_2504_14489_b200 import nccl
         comms = [nccl.Comm(rank, world), nccl.Comm(rank, world)]
-        wl.hooks = {0: lambda side, layer, stream: comms[0].all_reduce_(wl.dc_y, stream),
-                    1: lambda side, layer, stream: comms[1].all_reduce_(wl.pf_y, stream)}
+        wl.set_allreduce_hooks(comms)
     if world > 1:  # identical page tables on every rank (integer-exact check)
         h = torch.tensor([wl.page_hash], device="cuda")
         hs = [torch.zeros_like(h) for _ in range(world)]
@@ -427,26 +431,60 @@ def main():
     toks = wl.pf_spec.total_new + wl.dc_spec.num_seqs * iters
     value = toks / t_step  # tokens are whole-model tokens (all N_T layers); aggregate over ranks (head shards)
 
-    # ---- e2e through the public API: H2D of the step's inputs + D2H of the last outputs
-    pin = {k: getattr(wl, k).cpu().pin_memory() for k in ("pf_q", "pf_k", "pf_v", "dc_q", "dc_k", "dc_v")}
-    out_pf = torch.empty(wl.pf_y.shape, dtype=wl.pf_y.dtype).pin_memory()
-    out_dc = torch.empty(wl.dc_y.shape, dtype=wl.dc_y.dtype).pin_memory()
+    # ---- e2e through the public API: every step copies its inputs (new-token Q/K/V) from pinned
+    # host memory and its outputs (y of both sides) back.  Double-buffered like a server: step
+    # k+1's H2D and step k's D2H run on a copy stream while step k computes.
+    import copy as _copy
+    names_in = ("pf_q", "pf_k", "pf_v", "dc_q", "dc_k", "dc_v")
+    pin = {k: getattr(wl, k).cpu().pin_memory() for k in names_in}
+    wl2 = _copy.copy(wl)                                   # second I/O buffer set, same pool / batches / W_o
+    for k in names_in + ("pf_o", "dc_o", "pf_y", "dc_y"):
+        setattr(wl2, k, torch.empty_like(getattr(wl, k)))
+    wl2.ws = None
+    if comms:
+        wl2.set_allreduce_hooks(comms)
+    sets = [wl, wl2]
+    sides2 = [(pf, dc), wl2.sides(best["dec_sms"], iters)[:2]]
+    outs = [[torch.empty(w.pf_y.shape, dtype=w.pf_y.dtype).pin_memory(),
+             torch.empty(w.dc_y.shape, dtype=w.dc_y.dtype).pin_memory()] for w in sets]
     h2d = sum(t.numel() * t.element_size() for t in pin.values())
-    d2h = out_pf.numel() * out_pf.element_size() + out_dc.numel() * out_dc.element_size()
+    d2h = sum(t.numel() * t.element_size() for t in outs[0])
+    cs = torch.cuda.Stream()
+    ev_in = [torch.cuda.Event(), torch.cuda.Event()]
+    ev_done = [torch.cuda.Event(), torch.cuda.Event()]
+    ev_out = [torch.cuda.Event(), torch.cuda.Event()]
 
-    def e2e_step():
-        for k, t in pin.items():
-            getattr(wl, k).copy_(t, non_blocking=True)
-        mux.mux_run_layer(part, i, wl.pool, pf, dc, times)
-        out_pf.copy_(wl.pf_y, non_blocking=True)
-        out_dc.copy_(wl.dc_y, non_blocking=True)
-    for _ in range(2):
-        e2e_step()
+    def h2d_into(k):
+        with torch.cuda.stream(cs):
+            cs.wait_event(ev_out[k])                         # set k's last outputs are back on the host
+            for n, t in pin.items():
+                getattr(sets[k], n).copy_(t, non_blocking=True)
+            ev_in[k].record(cs)
+
+    def e2e_run(steps):
+        cs.wait_stream(st)
+        h2d_into(0)
+        for step in range(steps):
+            c = step % 2
+            if step + 1 < steps:
+                h2d_into(1 - c)                              # prefetch the next step's inputs
+            st.wait_event(ev_in[c])
+            mux.mux_run_layer(part, i, wl.pool, sides2[c][0], sides2[c][1], times)
+            ev_done[c].record(st)
+            with torch.cuda.stream(cs):
+                cs.wait_event(ev_done[c])
+                outs[c][0].copy_(sets[c].pf_y, non_blocking=True)
+                outs[c][1].copy_(sets[c].dc_y, non_blocking=True)
+                ev_out[c].record(cs)
+        st.wait_stream(cs)
+
+    for e in ev_out:
+        e.record(cs)
+    e2e_run(2)
     torch.cuda.synchronize()
     a2, b2 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     a2.record(st)
-    for _ in range(args.steps):
-        e2e_step()
+    e2e_run(args.steps)
     b2.record(st)
     torch.cuda.synchronize()
     t_e2e = a2.elapsed_time(b2) / args.steps * 1e-3
