@@ -20,7 +20,12 @@ t0 = t[t > 0].min()
 t = np.where(t > 0, t - t0, -1)
 print("tile  kload  vload")
 for j in range(56, 64): print(j, t[10, j], t[11, j])
-print("u swait0 sfull0 pass1_0 exp0 pfull0 | qk0 qkret0 pv0 || sfull1 pass1_1 exp1 pfull1 | qk1 pv1")
-for u in range(100, 128):
-    print(u, t[15, u], t[0, u], t[2, u], t[12, u], t[4, u], "|", t[8, u], t[14, u], t[6, u], "||",
-          t[1, u], t[3, u], t[13, u], t[5, u], "|", t[9, u], t[7, u])
+if os.environ.get("V6"):
+    print("j | qkA sfullA passA expA pvA || qkB sfullB passB expB pvB")
+    for j in range(50, 64):
+        print(j, "|", t[8, j], t[0, j], t[2, j], t[12, j], t[6, j], "||", t[9, j], t[1, j], t[3, j], t[13, j], t[7, j])
+else:
+    print("u swait0 sfull0 pass1_0 exp0 pfull0 | qk0 qkret0 pv0 || sfull1 pass1_1 exp1 pfull1 | qk1 pv1")
+    for u in range(100, 128):
+        print(u, t[15, u], t[0, u], t[2, u], t[12, u], t[4, u], "|", t[8, u], t[14, u], t[6, u], "||",
+              t[1, u], t[3, u], t[13, u], t[5, u], "|", t[9, u], t[7, u])
