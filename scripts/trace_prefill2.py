@@ -21,9 +21,10 @@ t = np.where(t > 0, t - t0, -1)
 print("tile  kload  vload")
 for j in range(56, 64): print(j, t[10, j], t[11, j])
 if os.environ.get("V6"):
-    print("j | qkA sfullA passA expA pvA || qkB sfullB passB expB pvB")
+    print("j | qkA sfullA passA expA pvA || qkB sfullB passB expB pvB || mma: wait_sfreeB seen | kload vload")
     for j in range(50, 64):
-        print(j, "|", t[8, j], t[0, j], t[2, j], t[12, j], t[6, j], "||", t[9, j], t[1, j], t[3, j], t[13, j], t[7, j])
+        print(j, "|", t[8, j], t[0, j], t[2, j], t[12, j], t[6, j], "||", t[9, j], t[1, j], t[3, j], t[13, j], t[7, j],
+              "||", t[14, j], t[15, j], "|", t[10, j], t[11, j])
 else:
     print("u swait0 sfull0 pass1_0 exp0 pfull0 | qk0 qkret0 pv0 || sfull1 pass1_1 exp1 pfull1 | qk1 pv1")
     for u in range(100, 128):
