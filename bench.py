@@ -515,7 +515,8 @@ def main():
                 "achieved": pf_tflops,
                 "peak": tc_peak, "unit": "TFLOP/s", "frac": pf_tflops / tc_peak,
                 "frac_of_sm_share": pf_tflops / (tc_peak * pf_share), "peak_src": f"{peaks_src} bf16_tflops_sustained",
-                "traffic": traffic.get("prefill_kernel", {}).get("bytes"),
+                "traffic": (traffic.get("prefill6_kernel") or traffic.get("prefill_kernel") or {}).get("bytes"),
+                "traffic_kernel": "prefill6_kernel" if "prefill6_kernel" in traffic else "prefill_kernel",
                 "per_launch": (f"1 layer: causal prefill attention {wl.prefill_flops_layer():.3e} FLOP + o_proj "
                                f"{wl.pf_spec.total_new}x{wl.Hq * wl.d}x{wl.hidden} {wl.outproj_flops_layer(wl.pf_spec):.3e}")}
     roofline_dec = {"bound": "hbm", "kernel": "decode_kernel", "achieved": dc_gbs, "peak": peaks["hbm_gbs"],
