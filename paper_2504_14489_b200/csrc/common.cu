@@ -64,7 +64,7 @@ int driver(const Driver** out) {
 }
 
 int make_tmap_bf16(CUtensorMap* map, const void* base, int rank, const uint64_t* dims,
-                   const uint64_t* strides_bytes, const uint32_t* box) {
+                   const uint64_t* strides_bytes, const uint32_t* box, bool swizzle) {
   const Driver* d;
   int rc = driver(&d);
   if (rc) return rc;
@@ -73,7 +73,8 @@ int make_tmap_bf16(CUtensorMap* map, const void* base, int rank, const uint64_t*
                                        reinterpret_cast<const cuuint64_t*>(dims),
                                        reinterpret_cast<const cuuint64_t*>(strides_bytes),
                                        reinterpret_cast<const cuuint32_t*>(box), elem_strides,
-                                       CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                                       CU_TENSOR_MAP_INTERLEAVE_NONE,
+                                       swizzle ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_NONE,
                                        CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) return cu_fail(r, "cuTensorMapEncodeTiled");
   return MUX_OK;

@@ -13,7 +13,9 @@
 // load of the row-major W fetched 128-byte rows 8 KiB apart and capped the skinny kernel at
 // ~40 GB/s per SM (ncu, profiles/r01_summary.md).
 //
-// Tile kernel (T > 128): persistent, one CTA per SM of the side's partition walking 128 x 256
+// Tile kernel (T > 128), default: CTA pairs (cta_group::2, below: 256 x 256 tiles, 1446 TF/s at
+// 8192x4096x4096 vs 1357 for the single-CTA kernel and 1515 for cuBLAS).  Single-CTA fallback:
+// persistent, one CTA per SM of the side's partition walking 128 x 256
 // output tiles, 6 warps: warp 4 = producer (TMA for X, bulk copies for W), warp 5 = TMEM owner
 // + single-thread tcgen05.mma issuer, warps 0-3 = epilogue (thread = output row).  4-stage ring
 // of {A: X 128 rows x 64 k (K-major, TMA SWIZZLE_128B), B: 2 packed W tiles = 64 k x 256 n
@@ -191,6 +193,139 @@ __global__ void __launch_bounds__(kGThreads, 1)
   if (warp == 5) {
     dev::tc_fence_after();
     dev::tmem_dealloc(tmem, 512);
+  }
+}
+
+// ---------------------------------------------------------------- CTA-pair tile kernel (T > 128)
+// A cluster of 2 CTAs (cta_group::2) computes one 256 x 256 output tile: each CTA loads its own
+// 128 rows of X and ONE packed 128-column W tile per k-block (32 KiB per stage instead of 48),
+// the leader CTA issues M=256 N=256 MMAs reading both CTAs' smem, and each CTA's TMEM holds its
+// 128 rows x 256 columns.  Per-SM smem fill per FLOP drops by a third.  Persistent over pairs;
+// both CTAs' loads complete on the leader's full barrier; the leader's commits multicast to
+// both CTAs' empty / accumulator barriers; the peer's epilogue releases an accumulator with a
+// remote arrive on the leader's barrier.
+constexpr int kP2Stages = 6;
+struct Gemm2Smem {
+  static constexpr int kA = kGBM * kGBK * 2;          // 16 KiB: my 128 rows x 64 k
+  static constexpr int kB = kPackTile;                // 16 KiB: my 128 columns x 64 k
+  static constexpr int kStage = kA + kB;
+  static constexpr int kBar = kP2Stages * kStage;
+  static constexpr int kTmemSlot = kBar + (2 * kP2Stages + 4) * 8;
+  static constexpr int kBytes = kTmemSlot + 16;
+};
+
+__global__ void __launch_bounds__(kGThreads, 1)
+    outproj2_kernel(const __grid_constant__ CUtensorMap tmap_x, const __grid_constant__ CUtensorMap tmap_w,
+                    const GemmParams p) {
+  using L = Gemm2Smem;
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + L::kBar);
+  uint64_t* empty = full + kP2Stages;
+  uint64_t* acc_full = empty + kP2Stages;
+  uint64_t* acc_empty = acc_full + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem + L::kTmemSlot);
+  const int warp = dev::warp_idx_uniform(), lane = threadIdx.x & 31;
+  const uint32_t rank = dev::cluster_ctarank();
+  const bool leader = rank == 0;
+  const int pair = blockIdx.x >> 1, npairs = gridDim.x >> 1;
+  const int nk = (p.K + kGBK - 1) / kGBK;
+  const int KB = nk;
+  const int ntiles128 = (p.N + 127) / 128;
+  const int tiles = p.m_tiles * p.n_tiles;        // m_tiles counts 256-row tiles here
+
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < 2 * kP2Stages + 2; ++i) dev::mbar_init(&full[i], 1);
+    dev::mbar_init(&acc_empty[0], 8);             // 4 epilogue warps x 2 CTAs (leader's copy is used)
+    dev::mbar_init(&acc_empty[1], 8);
+    dev::fence_mbar_init();
+  }
+  if (warp == 5) dev::tmem_alloc_pair(tmem_slot, 512);
+  dev::tc_fence_before();
+  __syncthreads();
+  dev::cluster_sync();                            // both CTAs' barriers exist before any remote use
+  dev::tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+  const uint32_t full_leader = dev::mapa(dev::smem_u32(full), 0);
+  const uint32_t acc_empty_leader = dev::mapa(dev::smem_u32(acc_empty), 0);
+
+  if (warp == 4) {
+    if (lane == 0) {
+      dev::tma_prefetch(&tmap_x);
+      dev::tma_prefetch(&tmap_w);
+      int it = 0;
+      for (int t = pair; t < tiles; t += npairs) {
+        const int m0 = (t / p.n_tiles) * 2 * kGBM + static_cast<int>(rank) * kGBM;
+        const int wt = (t % p.n_tiles) * 2 + static_cast<int>(rank);   // my packed 128-column tile
+        const int wtile = wt < ntiles128 ? wt : ntiles128 - 1;          // N tail: any valid tile (not stored)
+        for (int kb = 0; kb < nk; ++kb, ++it) {
+          const int s = it % kP2Stages;
+          if (it >= kP2Stages) dev::mbar_wait_sleep(&empty[s], ((it / kP2Stages) - 1) & 1);
+          if (leader) dev::mbar_expect_tx(&full[s], 2 * L::kStage);      // both CTAs' bytes
+          uint8_t* a = smem + s * L::kStage;
+          const uint32_t fb = full_leader + s * 8;
+          dev::tma_load_3d_pair(a, &tmap_x, fb, kb * kGBK, m0, 0);
+          dev::tma_load_3d_pair(a + L::kA, &tmap_w, fb, 0, 0, wtile * KB + kb);
+        }
+      }
+    }
+  } else if (warp == 5) {
+    if (lane == 0 && leader) {
+      constexpr uint32_t idesc = dev::umma_idesc_bf16(2 * kGBM, kGBN, 0, 1);
+      const uint64_t d0 = dev::umma_desc_sw128(dev::smem_u32(smem), 16, 1024);                   // A K-major
+      const uint64_t e0 = dev::umma_desc_sw128(dev::smem_u32(smem + L::kA), kGBK * 128, 1024);  // B MN-major
+      int it = 0, i = 0;
+      for (int t = pair; t < tiles; t += npairs, ++i) {
+        const int b = i & 1;
+        if (i >= 2) dev::mbar_wait_sleep(&acc_empty[b], ((i >> 1) - 1) & 1);
+        dev::tc_fence_after();
+        const uint32_t acc = tmem + b * kGBN;
+        for (int kb = 0; kb < nk; ++kb, ++it) {
+          const int s = it % kP2Stages;
+          dev::mbar_wait_sleep(&full[s], (it / kP2Stages) & 1);
+          dev::tc_fence_after();
+#pragma unroll
+          for (int kk = 0; kk < kGBK / 16; ++kk)
+            dev::umma_ss_pair(acc, d0 + ((s * L::kStage + kk * 32) >> 4), e0 + ((s * L::kStage + kk * 16 * 128) >> 4),
+                              idesc, (kb > 0 || kk > 0) ? 1u : 0u);
+          dev::umma_commit_pair(&empty[s]);
+        }
+        dev::umma_commit_pair(&acc_full[b]);
+      }
+    }
+    __syncwarp();
+  } else {
+    // epilogue (both CTAs): my 128 rows x 256 columns of TMEM buffer b
+    int i = 0;
+    for (int t = pair; t < tiles; t += npairs, ++i) {
+      const int b = i & 1;
+      const int m0 = (t / p.n_tiles) * 2 * kGBM + static_cast<int>(rank) * kGBM;
+      const int n0 = (t % p.n_tiles) * kGBN;
+      const int ncols = n0 + 128 < p.N ? kGBN : 128;
+      dev::mbar_wait_sleep(&acc_full[b], (i >> 1) & 1);
+      dev::tc_fence_after();
+      const int row = m0 + warp * 32 + lane;
+      const uint32_t taddr = tmem + b * kGBN + (static_cast<uint32_t>(warp * 32) << 16);
+#pragma unroll 1
+      for (int c = 0; c < kGBN / 32; ++c) {
+        uint32_t v[32];
+        dev::tmem_ld32(taddr + c * 32, v);
+        dev::tmem_wait_ld();
+        if (c == kGBN / 32 - 1) {
+          dev::tc_fence_before();
+          __syncwarp();
+          if (lane == 0) dev::mbar_arrive_cluster(acc_empty_leader + b * 8);
+        }
+        if (c * 32 < ncols) store_row32(p, row, n0 + c * 32, v);
+      }
+    }
+  }
+  dev::tc_fence_before();
+  __syncthreads();
+  dev::cluster_sync();
+  if (warp == 5) {
+    dev::tc_fence_after();
+    dev::tmem_dealloc_pair(tmem, 512);
   }
 }
 
@@ -390,6 +525,43 @@ int outproj_launch(const void* x, const void* w, void* y, int32_t y_dtype, int32
   uint32_t bx[3] = {kGBK, kGBM, 1};
   int rc = make_tmap_bf16(&tx, x, 3, dx, sx, bx);
   if (rc) return rc;
+  static const bool single_only = getenv("MUX_OUTPROJ_SINGLE") != nullptr;  // developer A/B switch
+  const int sms_avail = num_sms > 0 ? num_sms : device_sm_count();
+  if (!single_only && sms_avail >= 2) {
+    // packed W as {64 elements, 128 rows, tiles}: one box = one 16 KiB tile image (no swizzle:
+    // the image is already in the SWIZZLE_128B layout)
+    const int KB = (K + kGBK - 1) / kGBK, NT = (N + 127) / 128;
+    CUtensorMap tw;
+    uint64_t dw[3] = {64, 128, static_cast<uint64_t>(KB) * NT};
+    uint64_t sw[2] = {128, 16384};
+    uint32_t bw[3] = {64, 128, 1};
+    if ((rc = make_tmap_bf16(&tw, w, 3, dw, sw, bw, false))) return rc;
+    static bool attr2 = false;
+    const int smem2 = Gemm2Smem::kBytes + 1024;
+    if (!attr2) {
+      MUX_CUDA(cudaFuncSetAttribute(outproj2_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem2));
+      attr2 = true;
+    }
+    GemmParams prm{y, wp, T, N, K, y_dtype == MUX_DTYPE_F32, (T + 2 * kGBM - 1) / (2 * kGBM), (N + kGBN - 1) / kGBN};
+    const int tiles = prm.m_tiles * prm.n_tiles;
+    const int sms = num_sms > 0 ? num_sms : device_sm_count();
+    const int pairs = std::max(1, std::min(tiles, sms / 2));
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(2 * pairs);
+    cfg.blockDim = dim3(kGThreads);
+    cfg.dynamicSmemBytes = smem2;
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = 2;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    const cudaError_t e = cudaLaunchKernelEx(&cfg, outproj2_kernel, tx, tw, prm);
+    if (e == cudaSuccess) return MUX_OK;
+    (void)cudaGetLastError();  // no CTA pairs on this partition: fall back to the single-CTA kernel
+  }
   static bool attr_done = false;
   const int smem = GemmSmem::kBytes + 1024;
   if (!attr_done) {
