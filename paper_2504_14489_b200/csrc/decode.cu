@@ -33,8 +33,8 @@ namespace mux {
 namespace {
 
 constexpr int kConsumerWarps = 8;
-constexpr int kDecodeThreads = (kConsumerWarps + 1) * 32;
-constexpr int kRingBytes = 192 * 1024;   // K+V page stages in flight per CTA (1 CTA / SM)
+constexpr int kDecodeThreads = (kConsumerWarps + 2) * 32;   // + K producer + V producer
+constexpr int kRingBytes = 192 * 1024;   // K and V page stages in flight per CTA (1 CTA / SM)
 
 struct DecodeParams {
   const uint16_t* q;         // [B][Hq][D]
@@ -53,25 +53,27 @@ struct DecodeParams {
   float scale_log2;
 };
 
-// Stage = one page (16 tokens) of K and V for the HG kv heads of this CTA's group, as
-// TMA lands it: [HG][d/64][16 rows][128 B] (SWIZZLE_128B), K block then V block.
+// Two rings of stages, K and V: a stage = one page (16 tokens) of K (or V) for the HG kv heads
+// of this CTA's group, as TMA lands it: [HG][d/64][16 rows][128 B] (SWIZZLE_128B).  A K stage
+// is released right after QK (before the page's PV), so K refills run ahead of V.
 template <int D, int NT, int HG>
 struct DecodeSmem {
   static constexpr int kHeadBytes = D * kPage * 2;             // one (page, head) block of K (or V)
-  static constexpr int kStageBytes = 2 * HG * kHeadBytes;      // K + V of HG heads
+  static constexpr int kStageBytes = HG * kHeadBytes;          // K (or V) of HG heads
   static constexpr int kQStride = D + 8;                       // padded bf16 row -> conflict-free ldmatrix
   static constexpr int kQRowsPerHead = 8 * NT;                 // g <= 8*NT
   static constexpr int kQBytes = HG * kQRowsPerHead * kQStride * 2;
   static constexpr int kRing = (kRingBytes < 224 * 1024 - kQBytes) ? kRingBytes : 224 * 1024 - kQBytes;
-  static constexpr int kStages = (kRing / kStageBytes) > 24 ? 24 : (kRing / kStageBytes);
-  static constexpr int kQOff = kStages * kStageBytes;
+  static constexpr int kStages = (kRing / 2 / kStageBytes) > 12 ? 12 : (kRing / 2 / kStageBytes);   // per ring
+  static constexpr int kVOff = kStages * kStageBytes;
+  static constexpr int kQOff = 2 * kStages * kStageBytes;
   static constexpr int kBarOff = kQOff + kQBytes;
-  static constexpr int kBytes = kBarOff + 2 * kStages * 8;
+  static constexpr int kBytes = kBarOff + 4 * kStages * 8;
   // merge area (aliases the stage ring after the main loop): per warp 16 heads x D f32 + m, l
   static constexpr int kMergeM = kConsumerWarps * 16 * D * 4;
   static constexpr int kMergeL = kMergeM + kConsumerWarps * 16 * 4;
   static_assert(kStages >= 2, "ring too small");
-  static_assert(kMergeL + kConsumerWarps * 16 * 4 <= kStages * kStageBytes, "merge area too big");
+  static_assert(kMergeL + kConsumerWarps * 16 * 4 <= 2 * kStages * kStageBytes, "merge area too big");
 };
 
 template <int D, int NT, int HG>
@@ -83,8 +85,10 @@ __global__ void __launch_bounds__(kDecodeThreads, 1)
   constexpr int kWarpsPerHead = kConsumerWarps / HG;  // warps sharing one head split its pages
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  uint64_t* full = reinterpret_cast<uint64_t*>(smem + L::kBarOff);
-  uint64_t* empty = full + STAGES;
+  uint64_t* kfull = reinterpret_cast<uint64_t*>(smem + L::kBarOff);
+  uint64_t* kempty = kfull + STAGES;
+  uint64_t* vfull = kempty + STAGES;
+  uint64_t* vempty = vfull + STAGES;
   uint16_t* qs = reinterpret_cast<uint16_t*>(smem + L::kQOff);
 
   const int split = blockIdx.x, grp = blockIdx.y, b = blockIdx.z;
@@ -103,8 +107,10 @@ __global__ void __launch_bounds__(kDecodeThreads, 1)
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < STAGES; ++s) {
-      dev::mbar_init(&full[s], 1);
-      dev::mbar_init(&empty[s], HG);   // every head's consuming warp releases the stage
+      dev::mbar_init(&kfull[s], 1);
+      dev::mbar_init(&kempty[s], HG);  // every head's consuming warp releases the stage
+      dev::mbar_init(&vfull[s], 1);
+      dev::mbar_init(&vempty[s], HG);
     }
     dev::fence_mbar_init();
   }
@@ -133,12 +139,15 @@ __global__ void __launch_bounds__(kDecodeThreads, 1)
     for (int mt = 0; mt < D / 16; ++mt) oacc[mt][nt][0] = oacc[mt][nt][1] = oacc[mt][nt][2] = oacc[mt][nt][3] = 0.f;
   }
 
-  if (warp == kConsumerWarps) {
-    // ------------------------------------------------------------ producer: 2 TMA ops per page
-    if (lane == 0) {
-      dev::tma_prefetch(&tmap_k);
-      dev::tma_prefetch(&tmap_v);
-    }
+  if (warp >= kConsumerWarps) {
+    // ------------------------------------------------------------ producers: warp 8 K, warp 9 V,
+    // one TMA op per page each, independent rings
+    const bool is_v = warp == kConsumerWarps + 1;
+    const CUtensorMap* map = is_v ? &tmap_v : &tmap_k;
+    uint64_t* full = is_v ? vfull : kfull;
+    uint64_t* empty = is_v ? vempty : kempty;
+    uint8_t* ring = smem + (is_v ? L::kVOff : 0);
+    if (lane == 0) dev::tma_prefetch(map);
     int ids = 0;
     for (int i = 0; i < n_my; ++i) {
       if ((i & 31) == 0) ids = (pg0 + i + lane < pg1) ? __ldg(ptab + pg0 + i + lane) : 0;
@@ -147,9 +156,7 @@ __global__ void __launch_bounds__(kDecodeThreads, 1)
       if (lane == 0) {
         if (i >= STAGES) dev::mbar_wait(&empty[s], ((i / STAGES) - 1) & 1);
         dev::mbar_expect_tx(&full[s], L::kStageBytes);
-        uint8_t* kdst = smem + s * L::kStageBytes;
-        dev::tma_load_5d(kdst, &tmap_k, &full[s], 0, 0, 0, grp * HG, p.page_row0 + page);
-        dev::tma_load_5d(kdst + HG * L::kHeadBytes, &tmap_v, &full[s], 0, 0, 0, grp * HG, p.page_row0 + page);
+        dev::tma_load_5d(ring + s * L::kStageBytes, map, &full[s], 0, 0, 0, grp * HG, p.page_row0 + page);
       }
     }
   } else {
@@ -169,19 +176,11 @@ __global__ void __launch_bounds__(kDecodeThreads, 1)
     const int g4 = lane >> 2;
     for (int i = pl; i < n_my; i += kWarpsPerHead) {
       const int s = i % STAGES;
-      dev::mbar_wait(&full[s], (i / STAGES) & 1);
+      dev::mbar_wait(&kfull[s], (i / STAGES) & 1);
       uint8_t* kbuf = smem + s * L::kStageBytes + hw * L::kHeadBytes;
-      uint8_t* vbuf = kbuf + HG * L::kHeadBytes;
+      uint8_t* vbuf = smem + L::kVOff + s * L::kStageBytes + hw * L::kHeadBytes;
       const int pos0 = (pg0 + i) * kPage;
       const int valid = min(kPage, kv_len - pos0);
-      if (valid < kPage) {
-        // slots past the sequence end may hold anything (NaN-poisoned in tests): zero this
-        // head's V rows so P = 0 never meets NaN in the PV MMA; K rows are masked by select.
-        for (int r = valid; r < kPage; ++r)
-          for (int c = lane; c < (D / 64) * 8; c += 32)
-            *reinterpret_cast<uint4*>(vbuf + (c >> 3) * 2048 + r * 128 + (c & 7) * 16) = make_uint4(0, 0, 0, 0);
-        __syncwarp();
-      }
       // ---- S^T[16 tok x 8 heads] = K . Q^T
       float sacc[NT][4];
 #pragma unroll
@@ -214,9 +213,13 @@ __global__ void __launch_bounds__(kDecodeThreads, 1)
           mx0 = fmaxf(mx0, __shfl_xor_sync(0xffffffffu, mx0, off));
           mx1 = fmaxf(mx1, __shfl_xor_sync(0xffffffffu, mx1, off));
         }
-        const float mn0 = fmaxf(m_run[nt][0], mx0), mn1 = fmaxf(m_run[nt][1], mx1);  // finite: valid >= 1
-        alpha[nt][0] = dev::ex2(m_run[nt][0] - mn0);
-        alpha[nt][1] = dev::ex2(m_run[nt][1] - mn1);
+        // lazy rescale (FA4-style): the reference max moves only when the page max exceeds it by
+        // more than 8 (P <= 2^8 stays exact enough in P_hi + P_lo); otherwise alpha = 1 and the
+        // O rescale below is skipped for the whole warp
+        const float mn0 = (mx0 > m_run[nt][0] + 8.f) ? mx0 : m_run[nt][0];   // finite after page 0: valid >= 1
+        const float mn1 = (mx1 > m_run[nt][1] + 8.f) ? mx1 : m_run[nt][1];
+        alpha[nt][0] = (mn0 != m_run[nt][0]) ? dev::ex2(m_run[nt][0] - mn0) : 1.f;
+        alpha[nt][1] = (mn1 != m_run[nt][1]) ? dev::ex2(m_run[nt][1] - mn1) : 1.f;
         m_run[nt][0] = mn0;
         m_run[nt][1] = mn1;
         const float p0 = dev::ex2(x[0] - mn0), p1 = dev::ex2(x[1] - mn1);
@@ -232,7 +235,22 @@ __global__ void __launch_bounds__(kDecodeThreads, 1)
         plo[nt][0] = dev::movmatrix_t(l01);
         plo[nt][1] = dev::movmatrix_t(l23);
       }
+      __syncwarp();
+      if (lane == 0) dev::mbar_arrive(&kempty[s]);     // K page consumed: its stage may refill
+      dev::mbar_wait(&vfull[s], (i / STAGES) & 1);
+      if (valid < kPage) {
+        // slots past the sequence end may hold anything (NaN-poisoned in tests): zero this
+        // head's V rows so P = 0 never meets NaN in the PV MMA; K rows are masked by select.
+        for (int r = valid; r < kPage; ++r)
+          for (int c = lane; c < (D / 64) * 8; c += 32)
+            *reinterpret_cast<uint4*>(vbuf + (c >> 3) * 2048 + r * 128 + (c & 7) * 16) = make_uint4(0, 0, 0, 0);
+        __syncwarp();
+      }
       // ---- O^T = alpha * O^T + V^T . (P_hi + P_lo)^T
+      bool rescale = false;
+#pragma unroll
+      for (int nt = 0; nt < NT; ++nt) rescale |= (alpha[nt][0] != 1.f) | (alpha[nt][1] != 1.f);
+      rescale = __any_sync(0xffffffffu, rescale);
       const uint32_t vbase = dev::smem_u32(vbuf);
 #pragma unroll
       for (int mt = 0; mt < D / 16; ++mt) {
@@ -243,16 +261,18 @@ __global__ void __launch_bounds__(kDecodeThreads, 1)
         dev::ldsm_x4_t(vbase + (chunk >> 3) * 2048 + dev::sw128(tok, chunk & 7), a0, a1, a2, a3);
 #pragma unroll
         for (int nt = 0; nt < NT; ++nt) {
-          oacc[mt][nt][0] *= alpha[nt][0];
-          oacc[mt][nt][1] *= alpha[nt][1];
-          oacc[mt][nt][2] *= alpha[nt][0];
-          oacc[mt][nt][3] *= alpha[nt][1];
+          if (rescale) {
+            oacc[mt][nt][0] *= alpha[nt][0];
+            oacc[mt][nt][1] *= alpha[nt][1];
+            oacc[mt][nt][2] *= alpha[nt][0];
+            oacc[mt][nt][3] *= alpha[nt][1];
+          }
           dev::mma_bf16_16816(oacc[mt][nt], a0, a1, a2, a3, ph[nt][0], ph[nt][1]);
           dev::mma_bf16_16816(oacc[mt][nt], a0, a1, a2, a3, plo[nt][0], plo[nt][1]);
         }
       }
       __syncwarp();
-      if (lane == 0) dev::mbar_arrive(&empty[s]);
+      if (lane == 0) dev::mbar_arrive(&vempty[s]);
     }
 #pragma unroll
     for (int nt = 0; nt < NT; ++nt)

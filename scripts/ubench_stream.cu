@@ -89,6 +89,39 @@ __global__ void __launch_bounds__(288, 1) k_tma(const __grid_constant__ CUtensor
   }
 }
 
+// decode's pattern: one 5-D box = one page of 8 kv heads (8 x 4 KiB = 32 KiB), SWIZZLE_128B
+template <int STAGES, int NC>
+__global__ void __launch_bounds__(288, 1) k_tma32(const __grid_constant__ CUtensorMap map, int pages_per_cta,
+                                                  unsigned long long* sink) {
+  extern __shared__ __align__(1024) uint8_t sm_raw[];
+  uint8_t* sm = (uint8_t*)(((uintptr_t)sm_raw + 1023) & ~(uintptr_t)1023);   // SWIZZLE_128B needs 1 KiB alignment
+  constexpr int STAGE = 32768;
+  uint64_t* full = (uint64_t*)(sm + STAGES * STAGE);
+  uint64_t* empty = full + STAGES;
+  if (threadIdx.x == 0) { for (int i = 0; i < STAGES; ++i) { bar_init(&full[i], 1); bar_init(&empty[i], 1); } asm volatile("fence.mbarrier_init.release.cluster;"); }
+  __syncthreads();
+  unsigned long long acc = 0;
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < pages_per_cta; ++i) {
+      int s = i % STAGES;
+      if (i >= STAGES) wait(&empty[s], ((i / STAGES) - 1) & 1);
+      expect(&full[s], STAGE);
+      int page = blockIdx.x * pages_per_cta + i;
+      asm volatile("cp.async.bulk.tensor.5d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4, %5, %6}], [%7];"
+                   :: "r"(su32(sm + s * STAGE)), "l"((uint64_t)&map), "r"(0), "r"(0), "r"(0), "r"(0), "r"(page), "r"(su32(&full[s])) : "memory");
+    }
+  } else if ((threadIdx.x & 31) == 0 && threadIdx.x / 32 <= NC) {
+    const int w = threadIdx.x / 32 - 1;
+    for (int i = w; i < pages_per_cta; i += NC) {
+      int s = i % STAGES;
+      wait(&full[s], (i / STAGES) & 1);
+      acc += sm[s * STAGE + (i & 127)];
+      arrive(&empty[s]);
+    }
+    sink[blockIdx.x * 16 + w] = acc;
+  }
+}
+
 template <int UNROLL>
 __global__ void __launch_bounds__(512, 1) k_ldg(const uint4* src, size_t per_cta16, unsigned long long* sink) {
   const uint4* base = src + blockIdx.x * per_cta16;
@@ -127,6 +160,12 @@ int main(int argc, char** argv) {
   cuuint64_t strides5[4] = {256, 128, 4096, 8192};
   cuuint32_t box5[5] = {64, 16, 2, 1, 1}, es5[5] = {1, 1, 1, 1, 1};
   if (enc(&map5, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 5, buf, dims5, strides5, box5, es5, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS) { printf("encode5 failed\n"); return 1; }
+  CUtensorMap mapg;
+  const int total_pages32 = bytes / 32768;
+  cuuint64_t dimsg[5] = {64, 16, 2, 8, (cuuint64_t)total_pages32};
+  cuuint64_t stridesg[4] = {256, 128, 4096, 32768};
+  cuuint32_t boxg[5] = {64, 16, 2, 8, 1}, esg[5] = {1, 1, 1, 1, 1};
+  if (enc(&mapg, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 5, buf, dimsg, stridesg, boxg, esg, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS) { printf("encodeg failed\n"); return 1; }
   auto run = [&](const char* name, auto launch, int nsm, size_t moved) {
     launch(); CK(cudaDeviceSynchronize());
     cudaEventRecord(a); for (int r = 0; r < 3; ++r) launch(); cudaEventRecord(b); CK(cudaEventSynchronize(b));
@@ -143,6 +182,9 @@ int main(int argc, char** argv) {
 #define BULK(CH, ST, NC) if (++vid == only || only < 0) { auto k = k_bulk<CH, ST, NC>; int smem = ST * CH + 1024; cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, smem); \
       run("bulk " #CH " st" #ST " nc=" #NC, [&] { k<<<nsm, 288, smem>>>(buf, per, sink); }, nsm, (size_t)nsm * per); }
     BULK(4096, 48, 1) BULK(4096, 48, 8) BULK(8192, 24, 8) BULK(16384, 12, 8) BULK(32768, 6, 6) BULK(65536, 3, 3)
+#define TMA32(ST) if (++vid == only || only < 0) { auto k = k_tma32<ST, 6>; int smem = ST * 32768 + 2048; cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, smem); \
+      int pp32 = per / 32768; run("tma5d 32K-box st" #ST, [&] { k<<<nsm, 288, smem>>>(mapg, pp32, sink); }, nsm, (size_t)nsm * pp32 * 32768); }
+    TMA32(6) TMA32(3)
     if (++vid == only || only < 0) { auto k = k_ldg<8>;
       run("ldg.128 x8 512thr", [&] { k<<<nsm, 512>>>((const uint4*)buf, per / 16, sink); }, nsm, (size_t)nsm * per); }
   }
