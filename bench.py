@@ -277,7 +277,8 @@ def cpu_baseline_sample(config: int):
     from oracle.alloc import OraclePagePool, build_page_tables
     c = synth.get_config(config)
     S = c.shapes
-    dspec = SideSpec(c.decode.r[:4], c.decode.n[:4])
+    nd = 16                                   # sample: 16 decode sequences + 128 prefill rows (~10 s)
+    dspec = SideSpec(c.decode.r[:nd], c.decode.n[:nd])
     dside = synth.make_side(config, S, dspec, decode=True)
     pool = OraclePagePool(sum(dspec.pages_needed()) + 1, 1)
     ind, ids = build_page_tables(pool, dspec.pages_needed())
@@ -287,7 +288,7 @@ def cpu_baseline_sample(config: int):
     t0 = time.perf_counter()
     oracle.attention(dside.q, k, v, indptr(dspec.n), np.array(dspec.L, np.int32), np.array(ind, np.int32),
                      np.array(ids, np.int32), 1 / math.sqrt(S.d))
-    t_dec_tok = (time.perf_counter() - t0) / 4
+    t_dec_tok = (time.perf_counter() - t0) / nd
     pspec = c.prefill
     pside = synth.make_side(config, S, pspec, decode=False)
     pool = OraclePagePool(sum(pspec.pages_needed()) + 1, 1)
@@ -295,16 +296,21 @@ def cpu_baseline_sample(config: int):
     k, v = oracle.empty_pool(len(ids) + 1, S.Hkv, S.d, poison=False)
     oracle.append(k, v, np.concatenate(pside.k_rows), np.concatenate(pside.v_rows), indptr(pspec.L),
                   np.array(pspec.L, np.int32), np.array(ind, np.int32), np.array(ids, np.int32))
-    rows = synth.sample_rows(pspec.total_new, 32)
+    rows = synth.sample_rows(pspec.total_new, 128)
     t0 = time.perf_counter()
     oracle.attention(pside.q, k, v, indptr(pspec.n), np.array(pspec.L, np.int32), np.array(ind, np.int32),
                      np.array(ids, np.int32), 1 / math.sqrt(S.d), rows=rows)
-    t_pf_row = (time.perf_counter() - t0) / len(rows)
-    t_layer = c.decode.num_seqs * t_dec_tok + pspec.total_new * t_pf_row
+    t_pf = time.perf_counter() - t0
+    # a causal row's cost is proportional to the keys it attends: extrapolate by keys, not rows
+    key_of = np.concatenate([r + 1 + np.arange(n) for r, n in zip(pspec.r, pspec.n)])
+    t_pf_all = t_pf * float(key_of.sum()) / float(key_of[rows].sum())
+    t_dec_all = nd * t_dec_tok * sum(c.decode.L) / sum(dspec.L)          # decode cost ~ context
+    t_layer = t_dec_all + t_pf_all
     value = (pspec.total_new + c.decode.num_seqs) / (t_layer * S.n_layers_model)
     return {"value": value, "unit": "tok/s", "cores": oracle.num_threads(), "kind": "oracle",
-            "sample": f"4 decode seqs @ctx {c.decode.L[0]} + {len(rows)} sampled prefill rows (all heads, 1 layer), "
-                      f"extrapolated to 64 decodes + {pspec.total_new} prefill rows x {S.n_layers_model} layers"}
+            "sample": f"{nd} decode seqs @ctx {c.decode.L[0]} + {len(rows)} sampled prefill rows (all heads, 1 layer), "
+                      f"extrapolated by attended keys to {c.decode.num_seqs} decodes + {pspec.total_new} prefill rows "
+                      f"x {S.n_layers_model} layers"}
 
 
 # ----------------------------------------------------------------------------- main arm
