@@ -344,6 +344,18 @@ int mux_engine_request_pages(mux_engine_t eng, int32_t id, int32_t* kv_len, int3
 int mux_engine_trace(mux_engine_t eng, int64_t* out, int32_t cap, int32_t* n);
 int mux_engine_destroy(mux_engine_t eng);
 
+/* ------------------------------------------------------------------------------------
+ * Read-bandwidth probe: the partition-level denominator of the decode roofline (SURVEY
+ * §8(d) "BW_read(k_d): a read-only streaming kernel measured in the same green context";
+ * decode is memory-intensive).  Streams floor(bytes / 32 KiB) chunks of `src`
+ * (device, 16-byte aligned, read only) into shared memory with 32 KiB bulk copies through a
+ * 6-stage ring per CTA, the access pattern and op size of the decode kernel's page stream,
+ * and does nothing else with the data.  Grid: `num_ctas` CTAs (one per SM of the partition
+ * the stream belongs to), chunk c read by CTA c mod num_ctas.  Asynchronous on `stream`;
+ * time it with events on that stream.  Errors: MUX_ERR_INVALID_ARG (null src, < 1 chunk,
+ * num_ctas < 1), MUX_ERR_CUDA. */
+int mux_stream_read(const void* src, size_t bytes, int32_t num_ctas, mux_stream_t stream);
+
 const char* mux_last_error(void);
 /* library version string, e.g. "mux-b200 0.1 sm_100a" */
 const char* mux_version(void);

@@ -112,6 +112,7 @@ def lib():
         "mux_partition_query": [c_p, c_i32, ctypes.POINTER(c_i32), ctypes.POINTER(c_i32), ctypes.POINTER(c_p),
                                 ctypes.POINTER(c_p)],
         "mux_partition_memory": [c_p, ctypes.POINTER(c_i64)],
+        "mux_stream_read": [c_p, c_sz, c_i32, c_p],
         "mux_run_layer": [c_p, c_i32, c_p, ctypes.POINTER(SideC), ctypes.POINTER(SideC), c_p, c_p],
         "mux_outproj": [c_p, c_p, c_p, c_i32, c_i32, c_i32, c_i32, c_p],
         "mux_outproj_pack_w": [c_p, c_p, c_i32, c_i32, c_p],
@@ -369,6 +370,15 @@ def mux_outproj(x, w: PackedW, y, stream=None):
 
 def mux_device_sm_count(device: int = 0) -> int:
     return int(lib().mux_device_sm_count(device))
+
+
+def mux_stream_read(src, num_ctas: int, stream=None, nbytes: int | None = None) -> int:
+    """Read-bandwidth probe (include/mux.h): stream `src` (a device tensor) through shared memory
+    with 32 KiB bulk copies on `num_ctas` CTAs.  `stream`: a raw cudaStream_t (e.g. a partition
+    stream from Partition.query) or None for torch's current stream.  Returns the bytes read."""
+    nb = (nbytes if nbytes is not None else src.numel() * src.element_size()) // 32768 * 32768
+    _check(lib().mux_stream_read(c_p(src.data_ptr()), nb, num_ctas, c_p(_stream(stream))))
+    return nb
 
 
 # ------------------------------------------------------------------------------ partitions

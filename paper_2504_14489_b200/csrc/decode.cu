@@ -32,8 +32,19 @@
 namespace mux {
 namespace {
 
-constexpr int kConsumerWarps = 8;
-constexpr int kDecodeThreads = (kConsumerWarps + 2) * 32;   // + K producer + V producer
+// Consumer warps per CTA and head_dim split.  Default: 8 warps, one per (kv head, page lane).
+// MUX_DEC_SPLITD=2 (A/B build switch, g <= 8 only): 16 warps, two per kv head, each owning half of
+// head_dim (its half of the QK reduction and of the O rows), the two partial score tiles exchanged
+// through shared memory behind a 64-thread named barrier.  Measured slower on B200 (cfg2 layer on
+// 16 SMs: 704 us vs 560; profiles/r01_summary.md), kept for the record and for later tuning.
+#ifndef MUX_DEC_SPLITD
+#define MUX_DEC_SPLITD 1
+#endif
+template <int NT> struct DecodeCfg {
+  static constexpr int kSplitD = (NT == 1 && MUX_DEC_SPLITD == 2) ? 2 : 1;   // warps per (head, page)
+  static constexpr int kConsumerWarps = 8 * kSplitD;
+  static constexpr int kThreads = (kConsumerWarps + 2) * 32;   // + K producer + V producer
+};
 constexpr int kRingBytes = 192 * 1024;   // K and V page stages in flight per CTA (1 CTA / SM)
 
 struct DecodeParams {
@@ -58,31 +69,47 @@ struct DecodeParams {
 // is released right after QK (before the page's PV), so K refills run ahead of V.
 template <int D, int NT, int HG>
 struct DecodeSmem {
+  using C = DecodeCfg<NT>;
   static constexpr int kHeadBytes = D * kPage * 2;             // one (page, head) block of K (or V)
   static constexpr int kStageBytes = HG * kHeadBytes;          // K (or V) of HG heads
   static constexpr int kQStride = D + 8;                       // padded bf16 row -> conflict-free ldmatrix
   static constexpr int kQRowsPerHead = 8 * NT;                 // g <= 8*NT
   static constexpr int kQBytes = HG * kQRowsPerHead * kQStride * 2;
-  static constexpr int kRing = (kRingBytes < 224 * 1024 - kQBytes) ? kRingBytes : 224 * 1024 - kQBytes;
-  static constexpr int kStages = (kRing / 2 / kStageBytes) > 12 ? 12 : (kRing / 2 / kStageBytes);   // per ring
+  // partial-score exchange of the head_dim halves: [pair][2 buffers][2 halves][32 lanes][4 f32]
+  static constexpr int kPairs = C::kConsumerWarps / C::kSplitD;
+  static constexpr int kXBytes = C::kSplitD > 1 ? kPairs * 2 * 2 * 32 * 16 : 0;
+  static constexpr int kRing = (kRingBytes < 224 * 1024 - kQBytes - kXBytes) ? kRingBytes
+                                                                             : 224 * 1024 - kQBytes - kXBytes;
+  // stages per ring; a multiple of the page lanes of a head (W): a warp takes every W-th page, and
+  // its successive waits on one stage's mbarrier must be successive phases (parity)
+  static constexpr int kW = kPairs / HG;
+  static constexpr int kStagesFit = (kRing / 2 / kStageBytes) > 16 ? 16 : (kRing / 2 / kStageBytes);
+  static constexpr int kStages = kStagesFit / kW * kW;
   static constexpr int kVOff = kStages * kStageBytes;
   static constexpr int kQOff = 2 * kStages * kStageBytes;
-  static constexpr int kBarOff = kQOff + kQBytes;
+  static constexpr int kXOff = kQOff + kQBytes;
+  // merge area (aliases the ring, Q and the exchange after the main loop): per pair 16 heads x D f32 + m, l
+  static constexpr int kMergeM = kPairs * 16 * D * 4;
+  static constexpr int kMergeL = kMergeM + kPairs * 16 * 4;
+  static constexpr int kMergeEnd = kMergeL + kPairs * 16 * 4;
+  static constexpr int kBarOff = (kXOff + kXBytes) > kMergeEnd ? (kXOff + kXBytes) : kMergeEnd;
   static constexpr int kBytes = kBarOff + 4 * kStages * 8;
-  // merge area (aliases the stage ring after the main loop): per warp 16 heads x D f32 + m, l
-  static constexpr int kMergeM = kConsumerWarps * 16 * D * 4;
-  static constexpr int kMergeL = kMergeM + kConsumerWarps * 16 * 4;
-  static_assert(kStages >= 2, "ring too small");
-  static_assert(kMergeL + kConsumerWarps * 16 * 4 <= 2 * kStages * kStageBytes, "merge area too big");
+  static_assert(kStages >= 2 && kStages % kW == 0, "ring too small");
+  static_assert(kBytes + 1024 <= 227 * 1024, "shared memory");
 };
 
 template <int D, int NT, int HG>
-__global__ void __launch_bounds__(kDecodeThreads, 1)
+__global__ void __launch_bounds__(DecodeCfg<NT>::kThreads, 1)
     decode_kernel(const __grid_constant__ CUtensorMap tmap_k, const __grid_constant__ CUtensorMap tmap_v,
                   const DecodeParams p) {
   using L = DecodeSmem<D, NT, HG>;
+  using C = DecodeCfg<NT>;
+  constexpr int kConsumerWarps = C::kConsumerWarps;
+  constexpr int kThreads = C::kThreads;
+  constexpr int SD = C::kSplitD;
+  constexpr int DH = D / SD;                       // head_dim columns owned by one warp
   constexpr int STAGES = L::kStages;
-  constexpr int kWarpsPerHead = kConsumerWarps / HG;  // warps sharing one head split its pages
+  constexpr int kWarpsPerHead = L::kW;             // page lanes: warps (pairs) sharing one head split its pages
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint64_t* kfull = reinterpret_cast<uint64_t*>(smem + L::kBarOff);
@@ -108,16 +135,16 @@ __global__ void __launch_bounds__(kDecodeThreads, 1)
   if (threadIdx.x == 0) {
     for (int s = 0; s < STAGES; ++s) {
       dev::mbar_init(&kfull[s], 1);
-      dev::mbar_init(&kempty[s], HG);  // every head's consuming warp releases the stage
+      dev::mbar_init(&kempty[s], HG * SD);  // every consuming warp of every head releases the stage
       dev::mbar_init(&vfull[s], 1);
-      dev::mbar_init(&vempty[s], HG);
+      dev::mbar_init(&vempty[s], HG * SD);
     }
     dev::fence_mbar_init();
   }
   // Q rows of the HG*g q heads of this group -> [HG][8*NT][D+8] padded smem; rows >= g are zero
   {
     const uint16_t* qsrc = p.q + (static_cast<size_t>(b) * p.hq + static_cast<size_t>(grp) * HG * p.g) * D;
-    for (int i = threadIdx.x; i < HG * L::kQRowsPerHead * (D / 8); i += kDecodeThreads) {
+    for (int i = threadIdx.x; i < HG * L::kQRowsPerHead * (D / 8); i += kThreads) {
       const int row = i / (D / 8), c = i % (D / 8);
       const int hh = row / L::kQRowsPerHead, r = row % L::kQRowsPerHead;
       uint4 v = make_uint4(0, 0, 0, 0);
@@ -127,20 +154,22 @@ __global__ void __launch_bounds__(kDecodeThreads, 1)
   }
   __syncthreads();
 
-  const int hw = warp % HG;            // kv head (within the group) of this consumer warp
-  const int pl = warp / HG;            // its page lane among the warps of that head
+  const int pair = warp / SD;             // (head, page lane) slot of this consumer warp
+  const int half = warp % SD;             // which head_dim half it owns
+  const int hw = pair % HG;               // kv head (within the group)
+  const int pl = pair / HG;               // its page lane among the pairs of that head
   float m_run[NT][2], l_run[NT][2];
-  float oacc[D / 16][NT][4];
+  float oacc[DH / 16][NT][4];
 #pragma unroll
   for (int nt = 0; nt < NT; ++nt) {
     m_run[nt][0] = m_run[nt][1] = -INFINITY;
     l_run[nt][0] = l_run[nt][1] = 0.f;
 #pragma unroll
-    for (int mt = 0; mt < D / 16; ++mt) oacc[mt][nt][0] = oacc[mt][nt][1] = oacc[mt][nt][2] = oacc[mt][nt][3] = 0.f;
+    for (int mt = 0; mt < DH / 16; ++mt) oacc[mt][nt][0] = oacc[mt][nt][1] = oacc[mt][nt][2] = oacc[mt][nt][3] = 0.f;
   }
 
   if (warp >= kConsumerWarps) {
-    // ------------------------------------------------------------ producers: warp 8 K, warp 9 V,
+    // ------------------------------------------------------------ producers: K and V warps,
     // one TMA op per page each, independent rings
     const bool is_v = warp == kConsumerWarps + 1;
     const CUtensorMap* map = is_v ? &tmap_v : &tmap_k;
@@ -161,40 +190,66 @@ __global__ void __launch_bounds__(kDecodeThreads, 1)
     }
   } else {
     // ------------------------------------------------------------ consumers
-    uint32_t qf[NT][D / 16][2];
+    // Q^T fragments of this warp's head_dim half (k-chunks [half*DH/16, (half+1)*DH/16))
+    uint32_t qf[NT][DH / 16][2];
 #pragma unroll
     for (int nt = 0; nt < NT; ++nt) {
 #pragma unroll
-      for (int kc = 0; kc < D / 16; kc += 2) {
+      for (int kc = 0; kc < DH / 16; kc += 2) {
         const int mi = lane >> 3;
         const int row = hw * L::kQRowsPerHead + nt * 8 + (lane & 7);
-        const int chunk = 2 * kc + mi;
+        const int chunk = 2 * (half * DH / 16 + kc) + mi;
         dev::ldsm_x4(dev::smem_u32(qs + row * L::kQStride + chunk * 8), qf[nt][kc][0], qf[nt][kc][1],
                      qf[nt][kc + 1][0], qf[nt][kc + 1][1]);
       }
     }
+    float4* xb = reinterpret_cast<float4*>(smem + L::kXOff) + pair * 2 * 2 * 32;   // [2 buf][2 half][32]
     const int g4 = lane >> 2;
-    for (int i = pl; i < n_my; i += kWarpsPerHead) {
+    int it = 0;
+    for (int i = pl; i < n_my; i += kWarpsPerHead, ++it) {
       const int s = i % STAGES;
       dev::mbar_wait(&kfull[s], (i / STAGES) & 1);
       uint8_t* kbuf = smem + s * L::kStageBytes + hw * L::kHeadBytes;
       uint8_t* vbuf = smem + L::kVOff + s * L::kStageBytes + hw * L::kHeadBytes;
       const int pos0 = (pg0 + i) * kPage;
       const int valid = min(kPage, kv_len - pos0);
-      // ---- S^T[16 tok x 8 heads] = K . Q^T
-      float sacc[NT][4];
+      // ---- partial S^T[16 tok x 8 heads] = K[:, half] . Q[:, half]^T, even / odd k-chunks apart
+      float sacc[NT][4], sacc2[NT][4];
 #pragma unroll
-      for (int nt = 0; nt < NT; ++nt) sacc[nt][0] = sacc[nt][1] = sacc[nt][2] = sacc[nt][3] = 0.f;
+      for (int nt = 0; nt < NT; ++nt)
+#pragma unroll
+        for (int e = 0; e < 4; ++e) sacc[nt][e] = sacc2[nt][e] = 0.f;
       const uint32_t kbase = dev::smem_u32(kbuf);
 #pragma unroll
-      for (int kc = 0; kc < D / 16; ++kc) {
+      for (int kc = 0; kc < DH / 16; ++kc) {
         const int mi = lane >> 3;
         const int tok = (lane & 7) + ((mi & 1) << 3);
-        const int chunk = 2 * kc + (mi >> 1);
+        const int chunk = 2 * (half * DH / 16 + kc) + (mi >> 1);
         uint32_t a0, a1, a2, a3;
         dev::ldsm_x4(kbase + (chunk >> 3) * 2048 + dev::sw128(tok, chunk & 7), a0, a1, a2, a3);
 #pragma unroll
-        for (int nt = 0; nt < NT; ++nt) dev::mma_bf16_16816(sacc[nt], a0, a1, a2, a3, qf[nt][kc][0], qf[nt][kc][1]);
+        for (int nt = 0; nt < NT; ++nt)
+          dev::mma_bf16_16816((kc & 1) ? sacc2[nt] : sacc[nt], a0, a1, a2, a3, qf[nt][kc][0], qf[nt][kc][1]);
+      }
+#pragma unroll
+      for (int nt = 0; nt < NT; ++nt)
+#pragma unroll
+        for (int e = 0; e < 4; ++e) sacc[nt][e] += sacc2[nt][e];
+      __syncwarp();
+      if (lane == 0) dev::mbar_arrive(&kempty[s]);     // K page consumed: its stage may refill
+      if constexpr (SD > 1) {
+        // full S = own half + partner's half, added in the same order by both warps (identical S)
+        float4* mine = xb + ((it & 1) * 2 + half) * 32 + lane;
+        float4* other = xb + ((it & 1) * 2 + (half ^ 1)) * 32 + lane;
+        *mine = make_float4(sacc[0][0], sacc[0][1], sacc[0][2], sacc[0][3]);
+        dev::named_bar_sync(1 + pair, 64);
+        const float4 o4 = *other;
+        const float lo[4] = {half ? o4.x : sacc[0][0], half ? o4.y : sacc[0][1], half ? o4.z : sacc[0][2],
+                             half ? o4.w : sacc[0][3]};
+        const float hi[4] = {half ? sacc[0][0] : o4.x, half ? sacc[0][1] : o4.y, half ? sacc[0][2] : o4.z,
+                             half ? sacc[0][3] : o4.w};
+#pragma unroll
+        for (int e = 0; e < 4; ++e) sacc[0][e] = lo[e] + hi[e];
       }
       // ---- online softmax (log2 domain); thread holds tokens g4, g4+8 x heads 2q, 2q+1
       const bool v0 = g4 < valid, v1 = (g4 + 8) < valid;
@@ -235,28 +290,28 @@ __global__ void __launch_bounds__(kDecodeThreads, 1)
         plo[nt][0] = dev::movmatrix_t(l01);
         plo[nt][1] = dev::movmatrix_t(l23);
       }
-      __syncwarp();
-      if (lane == 0) dev::mbar_arrive(&kempty[s]);     // K page consumed: its stage may refill
       dev::mbar_wait(&vfull[s], (i / STAGES) & 1);
       if (valid < kPage) {
-        // slots past the sequence end may hold anything (NaN-poisoned in tests): zero this
-        // head's V rows so P = 0 never meets NaN in the PV MMA; K rows are masked by select.
+        // slots past the sequence end may hold anything (NaN-poisoned in tests): zero this warp's
+        // V columns there so P = 0 never meets NaN in the PV MMA; K rows are masked by select.
         for (int r = valid; r < kPage; ++r)
-          for (int c = lane; c < (D / 64) * 8; c += 32)
-            *reinterpret_cast<uint4*>(vbuf + (c >> 3) * 2048 + r * 128 + (c & 7) * 16) = make_uint4(0, 0, 0, 0);
+          for (int c = lane; c < DH / 8; c += 32) {
+            const int cc = half * (DH / 8) + c;   // logical 16-byte column chunk of the head row
+            *reinterpret_cast<uint4*>(vbuf + (cc >> 3) * 2048 + dev::sw128(r, cc & 7)) = make_uint4(0, 0, 0, 0);
+          }
         __syncwarp();
       }
-      // ---- O^T = alpha * O^T + V^T . (P_hi + P_lo)^T
+      // ---- O^T[half] = alpha * O^T[half] + V^T[half] . (P_hi + P_lo)^T
       bool rescale = false;
 #pragma unroll
       for (int nt = 0; nt < NT; ++nt) rescale |= (alpha[nt][0] != 1.f) | (alpha[nt][1] != 1.f);
       rescale = __any_sync(0xffffffffu, rescale);
       const uint32_t vbase = dev::smem_u32(vbuf);
 #pragma unroll
-      for (int mt = 0; mt < D / 16; ++mt) {
+      for (int mt = 0; mt < DH / 16; ++mt) {
         const int mi = lane >> 3;
         const int tok = (lane & 7) + ((mi >> 1) << 3);
-        const int chunk = 2 * mt + (mi & 1);
+        const int chunk = 2 * (half * DH / 16 + mt) + (mi & 1);
         uint32_t a0, a1, a2, a3;
         dev::ldsm_x4_t(vbase + (chunk >> 3) * 2048 + dev::sw128(tok, chunk & 7), a0, a1, a2, a3);
 #pragma unroll
@@ -292,15 +347,15 @@ __global__ void __launch_bounds__(kDecodeThreads, 1)
 #pragma unroll
     for (int nt = 0; nt < NT; ++nt) {
       const int h0 = nt * 8 + 2 * q4;
-      if (g4 == 0) {
-        mm[warp * 16 + h0] = m_run[nt][0];
-        mm[warp * 16 + h0 + 1] = m_run[nt][1];
-        ml[warp * 16 + h0] = l_run[nt][0];
-        ml[warp * 16 + h0 + 1] = l_run[nt][1];
+      if (g4 == 0 && half == 0) {   // both halves hold the same m, l
+        mm[pair * 16 + h0] = m_run[nt][0];
+        mm[pair * 16 + h0 + 1] = m_run[nt][1];
+        ml[pair * 16 + h0] = l_run[nt][0];
+        ml[pair * 16 + h0 + 1] = l_run[nt][1];
       }
-      float* base = mo + (warp * 16) * D;
+      float* base = mo + (pair * 16) * D + half * DH;
 #pragma unroll
-      for (int mt = 0; mt < D / 16; ++mt) {
+      for (int mt = 0; mt < DH / 16; ++mt) {
         base[h0 * D + mt * 16 + g4] = oacc[mt][nt][0];
         base[(h0 + 1) * D + mt * 16 + g4] = oacc[mt][nt][1];
         base[h0 * D + mt * 16 + g4 + 8] = oacc[mt][nt][2];
@@ -309,8 +364,8 @@ __global__ void __launch_bounds__(kDecodeThreads, 1)
     }
   }
   __syncthreads();
-  // merge the warps of each head: element (head-in-group, q head, dim) per thread
-  for (int e = threadIdx.x; e < HG * p.g * D; e += kDecodeThreads) {
+  // merge the page lanes of each head: element (head-in-group, q head, dim) per thread
+  for (int e = threadIdx.x; e < HG * p.g * D; e += kThreads) {
     const int c = e % D, hq_in = (e / D) % p.g, hh = e / (D * p.g);
     float M = -INFINITY;
 #pragma unroll
@@ -386,7 +441,7 @@ int launch_decode_hg(mux_pool* pool, const DecodeParams& prm, int B, cudaStream_
     attr_done = true;
   }
   dim3 grid(prm.num_splits, prm.hkv / HG, B);
-  kern<<<grid, kDecodeThreads, smem, st>>>(pool->tmap_kg, pool->tmap_vg, prm);
+  kern<<<grid, DecodeCfg<NT>::kThreads, smem, st>>>(pool->tmap_kg, pool->tmap_vg, prm);
   MUX_CUDA(cudaGetLastError());
   if (prm.num_splits > 1) {
     combine_kernel<D><<<B * prm.hq, D, 0, st>>>(prm.part_o, prm.part_m, prm.part_l, prm.o, prm.lse, prm.kv_len,

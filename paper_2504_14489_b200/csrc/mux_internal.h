@@ -229,6 +229,10 @@ __device__ __forceinline__ uint32_t sw128(uint32_t row, uint32_t chunk) {
 }
 
 // ---------------------------------------------------------------- legacy tensor-core (decode)
+// named barrier over `count` threads (whole warps); id 0 is __syncthreads
+__device__ __forceinline__ void named_bar_sync(int id, int count) {
+  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(count) : "memory");
+}
 __device__ __forceinline__ void ldsm_x4(uint32_t addr, uint32_t& r0, uint32_t& r1, uint32_t& r2, uint32_t& r3) {
   asm volatile("ldmatrix.sync.aligned.m8n8.x4.shared.b16 {%0,%1,%2,%3}, [%4];"
                : "=r"(r0), "=r"(r1), "=r"(r2), "=r"(r3)

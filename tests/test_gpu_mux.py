@@ -41,6 +41,31 @@ def test_partition_grants(mux, part):
     assert part.memory_bytes() >= 0
 
 
+def test_stream_read_probe(mux, part):
+    """The decode roofline's partition denominator (mux_stream_read): runs on a partition stream
+    and on the whole GPU, more SMs read faster, bad arguments are rejected."""
+    import torch
+    buf = torch.zeros(256 << 20, dtype=torch.uint8, device="cuda")
+
+    def gbs(stream, sms):
+        st = torch.cuda.ExternalStream(stream) if stream else torch.cuda.current_stream()
+        mux.mux_stream_read(buf, sms, st)
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(st)
+        n = sum(mux.mux_stream_read(buf, sms, st) for _ in range(5))
+        b.record(st)
+        torch.cuda.synchronize()
+        return n / (a.elapsed_time(b) * 1e-3) / 1e9
+    d16, _, sd16, _ = part.query(0)
+    small, full = gbs(sd16, d16), gbs(None, mux.mux_device_sm_count(0))
+    assert 100 < small < full, (small, full)
+    assert full > 2000, full
+    with pytest.raises(mux.MuxError):
+        mux.mux_stream_read(buf, 0)
+    with pytest.raises(mux.MuxError):
+        mux.mux_stream_read(buf, 4, nbytes=1000)
+
+
 def _workload(mux, Hq=8, Hkv=2, d=128):
     import torch
     pf = make_side(801, Shapes(Hq, Hkv, d, 1), SideSpec([37, 0], [300, 129]), decode=False)

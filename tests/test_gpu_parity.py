@@ -87,6 +87,9 @@ DECODE_CASES = [
     (128, 64, 8, [33, 4096]),                          # g = 8 (70B)
     (64, 16, 1, [129, 48]),                            # g = 16 (two N tiles)
     (128, 8, 8, [513]),                                # MHA g = 1
+    (128, 4, 1, [3000, 17]),                           # one kv head: 8 warps share its pages (16-stage ring)
+    (64, 8, 2, [2100]),                                # g = 4, two kv heads per CTA
+    (128, 16, 8, [700, 1]),                            # g = 2
 ]
 
 
