@@ -553,6 +553,10 @@ def main():
                     "unit": "GB/s", "frac": dc_gbs / peaks["hbm_gbs"], "peak_src": f"{peaks_src} hbm_gbs",
                     "sm_share": dc_share, "partition_read_gbs": bw_part, "full_gpu_read_gbs": bw_full,
                     "frac_of_partition_read": dc_gbs / bw_part,
+                    # the same decode layer on the same partition with the prefill side idle (sweep)
+                    "iso_achieved": wl.decode_bytes_layer() / (best["t_dc_iso_ms"] * 1e-3 / wl.layers) / 1e9,
+                    "iso_frac_of_partition_read": wl.decode_bytes_layer() / (best["t_dc_iso_ms"] * 1e-3 / wl.layers)
+                    / 1e9 / bw_part,
                     "partition_read_src": f"mux_stream_read on the {best['dec_sms']}-SM decode partition (alone)",
                     "traffic": traffic.get("decode_kernel", {}).get("bytes")}
     launches_per_step = wl.layers * 3 + wl.layers * iters * (3 + (1 if ns > 1 else 0)) + 4
