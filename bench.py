@@ -532,13 +532,13 @@ def main():
     tc_peak = peaks.get("bf16_tflops_sustained", peaks["bf16_tflops"])
     traffic = {}
     try:
-        with open(os.path.join(ROOT, "profiles", "r01_traffic.json")) as f:
+        with open(os.path.join(ROOT, "profiles", "r01s2_traffic.json")) as f:
             traffic = json.load(f)
     except Exception:
         pass
     pf_share = best["pf_sms"] / total_sms
     dc_share = best["dec_sms"] / total_sms
-    roofline = {"bound": "tensor", "kernel": "prefill side per layer: prefill_kernel + outproj_kernel (tcgen05)",
+    roofline = {"bound": "tensor", "kernel": "prefill side per layer: prefill6_kernel + outproj2_kernel (tcgen05)",
                 "achieved": pf_tflops,
                 "peak": tc_peak, "unit": "TFLOP/s", "frac": pf_tflops / tc_peak,
                 "frac_of_sm_share": pf_tflops / (tc_peak * pf_share), "peak_src": f"{peaks_src} bf16_tflops_sustained",
