@@ -40,12 +40,16 @@ namespace {
 #ifndef MUX_DEC_SPLITD
 #define MUX_DEC_SPLITD 1
 #endif
+#ifndef MUX_DEC_2CTA
+#define MUX_DEC_2CTA 0   // A/B switch: two CTAs per SM (4 kv heads, 4 consumer warps, 96 KiB ring each)
+#endif
 template <int NT> struct DecodeCfg {
   static constexpr int kSplitD = (NT == 1 && MUX_DEC_SPLITD == 2) ? 2 : 1;   // warps per (head, page)
-  static constexpr int kConsumerWarps = 8 * kSplitD;
+  static constexpr int kConsumerWarps = MUX_DEC_2CTA ? 4 : 8 * kSplitD;
+  static constexpr int kCtasPerSm = MUX_DEC_2CTA ? 2 : 1;
   static constexpr int kThreads = (kConsumerWarps + 2) * 32;   // + K producer + V producer
 };
-constexpr int kRingBytes = 192 * 1024;   // K and V page stages in flight per CTA (1 CTA / SM)
+constexpr int kRingBytes = (MUX_DEC_2CTA ? 96 : 192) * 1024;   // K and V page stages in flight per CTA
 
 struct DecodeParams {
   const uint16_t* q;         // [B][Hq][D]
@@ -78,11 +82,11 @@ struct DecodeSmem {
   // partial-score exchange of the head_dim halves: [pair][2 buffers][2 halves][32 lanes][4 f32]
   static constexpr int kPairs = C::kConsumerWarps / C::kSplitD;
   static constexpr int kXBytes = C::kSplitD > 1 ? kPairs * 2 * 2 * 32 * 16 : 0;
-  static constexpr int kRing = (kRingBytes < 224 * 1024 - kQBytes - kXBytes) ? kRingBytes
-                                                                             : 224 * 1024 - kQBytes - kXBytes;
+  static constexpr int kSmemCap = (MUX_DEC_2CTA ? 112 : 224) * 1024;
+  static constexpr int kRing = (kRingBytes < kSmemCap - kQBytes - kXBytes) ? kRingBytes : kSmemCap - kQBytes - kXBytes;
   // stages per ring; a multiple of the page lanes of a head (W): a warp takes every W-th page, and
   // its successive waits on one stage's mbarrier must be successive phases (parity)
-  static constexpr int kW = kPairs / HG;
+  static constexpr int kW = kPairs / HG > 0 ? kPairs / HG : 1;
   static constexpr int kStagesFit = (kRing / 2 / kStageBytes) > 16 ? 16 : (kRing / 2 / kStageBytes);
   static constexpr int kStages = kStagesFit / kW * kW;
   static constexpr int kVOff = kStages * kStageBytes;
@@ -95,11 +99,11 @@ struct DecodeSmem {
   static constexpr int kBarOff = (kXOff + kXBytes) > kMergeEnd ? (kXOff + kXBytes) : kMergeEnd;
   static constexpr int kBytes = kBarOff + 4 * kStages * 8;
   static_assert(kStages >= 2 && kStages % kW == 0, "ring too small");
-  static_assert(kBytes + 1024 <= 227 * 1024, "shared memory");
+  static_assert(kBytes + 1024 <= kSmemCap + 3 * 1024, "shared memory");
 };
 
 template <int D, int NT, int HG>
-__global__ void __launch_bounds__(DecodeCfg<NT>::kThreads, 1)
+__global__ void __launch_bounds__(DecodeCfg<NT>::kThreads, DecodeCfg<NT>::kCtasPerSm)
     decode_kernel(const __grid_constant__ CUtensorMap tmap_k, const __grid_constant__ CUtensorMap tmap_v,
                   const DecodeParams p) {
   using L = DecodeSmem<D, NT, HG>;
@@ -454,7 +458,9 @@ int launch_decode_hg(mux_pool* pool, const DecodeParams& prm, int B, cudaStream_
 template <int D, int NT>
 int launch_decode(mux_pool* pool, const DecodeParams& prm, int B, cudaStream_t st) {
   switch (pool->hg) {
+#if !MUX_DEC_2CTA
     case 8: return launch_decode_hg<D, NT, 8>(pool, prm, B, st);
+#endif
     case 4: return launch_decode_hg<D, NT, 4>(pool, prm, B, st);
     case 2: return launch_decode_hg<D, NT, 2>(pool, prm, B, st);
     case 1: return launch_decode_hg<D, NT, 1>(pool, prm, B, st);
@@ -481,7 +487,7 @@ int32_t mux_decode_num_splits(int32_t num_seqs, int32_t hkv, int32_t head_dim, c
   if (num_sms < 1) num_sms = 148;
   if (head_dim < 1) head_dim = 128;
   int hg = 1;
-  for (int c = 1; c <= 8; ++c)
+  for (int c = 1; c <= (MUX_DEC_2CTA ? 4 : 8); ++c)
     if (hkv % c == 0) hg = c;
   const int groups = hkv / hg;
   const int max_pages = (max_kv + kPage - 1) / kPage;

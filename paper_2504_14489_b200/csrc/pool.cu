@@ -27,8 +27,11 @@ int pool_tmaps(mux_pool* p) {
   uint64_t dims[5] = {64, static_cast<uint64_t>(kPage), D / 64, static_cast<uint64_t>(d.num_kv_heads),
                       static_cast<uint64_t>(d.num_layers) * static_cast<uint64_t>(d.num_pages)};
   uint64_t strides[4] = {D * 2, 128, kPage * D * 2, static_cast<uint64_t>(d.num_kv_heads) * kPage * D * 2};
+#ifndef MUX_DEC_2CTA
+#define MUX_DEC_2CTA 0
+#endif
   int hg = 1;
-  for (int c = 1; c <= 8; ++c)
+  for (int c = 1; c <= (MUX_DEC_2CTA ? 4 : 8); ++c)   // kv heads per decode CTA (csrc/decode.cu)
     if (d.num_kv_heads % c == 0) hg = c;
   p->hg = hg;
   uint32_t box1[5] = {64, static_cast<uint32_t>(kPage), static_cast<uint32_t>(D / 64), 1, 1};
