@@ -259,30 +259,41 @@ __global__ void __launch_bounds__(DecodeCfg<NT>::kThreads, DecodeCfg<NT>::kCtasP
       const bool v0 = g4 < valid, v1 = (g4 + 8) < valid;
       uint32_t ph[NT][2], plo[NT][2];
       float alpha[NT][2];
+      float x[NT][4];
+      bool grow = false;   // does any score exceed its column's reference max by more than 8?
 #pragma unroll
       for (int nt = 0; nt < NT; ++nt) {
-        float x[4];
-        x[0] = v0 ? sacc[nt][0] * p.scale_log2 : -INFINITY;
-        x[1] = v0 ? sacc[nt][1] * p.scale_log2 : -INFINITY;
-        x[2] = v1 ? sacc[nt][2] * p.scale_log2 : -INFINITY;
-        x[3] = v1 ? sacc[nt][3] * p.scale_log2 : -INFINITY;
-        float mx0 = fmaxf(x[0], x[2]), mx1 = fmaxf(x[1], x[3]);
+        x[nt][0] = v0 ? sacc[nt][0] * p.scale_log2 : -INFINITY;
+        x[nt][1] = v0 ? sacc[nt][1] * p.scale_log2 : -INFINITY;
+        x[nt][2] = v1 ? sacc[nt][2] * p.scale_log2 : -INFINITY;
+        x[nt][3] = v1 ? sacc[nt][3] * p.scale_log2 : -INFINITY;
+        grow |= (fmaxf(x[nt][0], x[nt][2]) > m_run[nt][0] + 8.f) | (fmaxf(x[nt][1], x[nt][3]) > m_run[nt][1] + 8.f);
+      }
+      // lazy rescale (FA4-style): a column's reference max moves only when the page max exceeds it by
+      // more than 8 (P <= 2^8 stays exact enough in P_hi + P_lo); otherwise alpha = 1 and the O
+      // rescale below is skipped.  The exact page max (3 shuffle rounds per column on the page's
+      // critical path) is only needed when some column grows, which one warp vote tells (after the
+      // first page: rarely); the result is the same as always taking the max.
+      grow = __any_sync(0xffffffffu, grow);
 #pragma unroll
-        for (int off = 4; off < 32; off <<= 1) {
-          mx0 = fmaxf(mx0, __shfl_xor_sync(0xffffffffu, mx0, off));
-          mx1 = fmaxf(mx1, __shfl_xor_sync(0xffffffffu, mx1, off));
+      for (int nt = 0; nt < NT; ++nt) {
+        float mn0 = m_run[nt][0], mn1 = m_run[nt][1];
+        if (grow) {
+          float mx0 = fmaxf(x[nt][0], x[nt][2]), mx1 = fmaxf(x[nt][1], x[nt][3]);
+#pragma unroll
+          for (int off = 4; off < 32; off <<= 1) {
+            mx0 = fmaxf(mx0, __shfl_xor_sync(0xffffffffu, mx0, off));
+            mx1 = fmaxf(mx1, __shfl_xor_sync(0xffffffffu, mx1, off));
+          }
+          mn0 = (mx0 > m_run[nt][0] + 8.f) ? mx0 : m_run[nt][0];   // finite after page 0: valid >= 1
+          mn1 = (mx1 > m_run[nt][1] + 8.f) ? mx1 : m_run[nt][1];
         }
-        // lazy rescale (FA4-style): the reference max moves only when the page max exceeds it by
-        // more than 8 (P <= 2^8 stays exact enough in P_hi + P_lo); otherwise alpha = 1 and the
-        // O rescale below is skipped for the whole warp
-        const float mn0 = (mx0 > m_run[nt][0] + 8.f) ? mx0 : m_run[nt][0];   // finite after page 0: valid >= 1
-        const float mn1 = (mx1 > m_run[nt][1] + 8.f) ? mx1 : m_run[nt][1];
         alpha[nt][0] = (mn0 != m_run[nt][0]) ? dev::ex2(m_run[nt][0] - mn0) : 1.f;
         alpha[nt][1] = (mn1 != m_run[nt][1]) ? dev::ex2(m_run[nt][1] - mn1) : 1.f;
         m_run[nt][0] = mn0;
         m_run[nt][1] = mn1;
-        const float p0 = dev::ex2(x[0] - mn0), p1 = dev::ex2(x[1] - mn1);
-        const float p2 = dev::ex2(x[2] - mn0), p3 = dev::ex2(x[3] - mn1);
+        const float p0 = dev::ex2(x[nt][0] - mn0), p1 = dev::ex2(x[nt][1] - mn1);
+        const float p2 = dev::ex2(x[nt][2] - mn0), p3 = dev::ex2(x[nt][3] - mn1);
         l_run[nt][0] = l_run[nt][0] * alpha[nt][0] + p0 + p2;
         l_run[nt][1] = l_run[nt][1] * alpha[nt][1] + p1 + p3;
         // P = P_hi + P_lo, both bf16: ~16 significant bits
