@@ -317,10 +317,12 @@ __global__ void __launch_bounds__(DecodeCfg<NT>::kThreads, DecodeCfg<NT>::kCtasP
         __syncwarp();
       }
       // ---- O^T[half] = alpha * O^T[half] + V^T[half] . (P_hi + P_lo)^T
-      bool rescale = false;
+      bool rescale = false;   // alpha != 1 only where a column grew (so never without `grow`)
+      if (grow) {
 #pragma unroll
-      for (int nt = 0; nt < NT; ++nt) rescale |= (alpha[nt][0] != 1.f) | (alpha[nt][1] != 1.f);
-      rescale = __any_sync(0xffffffffu, rescale);
+        for (int nt = 0; nt < NT; ++nt) rescale |= (alpha[nt][0] != 1.f) | (alpha[nt][1] != 1.f);
+        rescale = __any_sync(0xffffffffu, rescale);
+      }
       const uint32_t vbase = dev::smem_u32(vbuf);
 #pragma unroll
       for (int mt = 0; mt < DH / 16; ++mt) {
