@@ -509,7 +509,10 @@ int32_t mux_decode_num_splits(int32_t num_seqs, int32_t hkv, int32_t head_dim, c
   // combine pass ~6 us + its partial traffic.  The grid's CTAs are dispatched in launch order
   // (split fastest) onto the first free SM; the split count with the smallest predicted
   // makespan wins.  Balanced splits: C = ceil(max_pages / S) pages per split for every sequence.
-  const double page_us = static_cast<double>(hg) * kPage * head_dim * 2 * 2 / 1.0e5;
+  // two CTAs share an SM under MUX_DEC_2CTA: twice the slots, each streaming about half as fast
+  const int slots = num_sms * DecodeCfg<1>::kCtasPerSm;
+  const double cta_bytes_per_us = DecodeCfg<1>::kCtasPerSm == 2 ? 6.5e4 : 1.0e5;
+  const double page_us = static_cast<double>(hg) * kPage * head_dim * 2 * 2 / cta_bytes_per_us;
   const double cta_us = 4.0, empty_us = 0.3;
   std::vector<int> pages(num_seqs);
   for (int i = 0; i < num_seqs; ++i) {
@@ -519,7 +522,7 @@ int32_t mux_decode_num_splits(int32_t num_seqs, int32_t hkv, int32_t head_dim, c
   int64_t total_pages = 0;
   for (int p : pages) total_pages += p;
   // ~6.5 TB/s measured copy bandwidth (MEASURED_PEAKS hbm_gbs), in bytes per us
-  const double hbm_floor_us = static_cast<double>(total_pages) * groups * page_us * 1.0e5 / 6.5e6;
+  const double hbm_floor_us = static_cast<double>(total_pages) * groups * page_us * cta_bytes_per_us / 6.5e6;
   static const int cands[] = {1, 2, 3, 4, 6, 8, 12, 16, 24, 32, 48, 64};
   int best_s = 1;
   double best_t = 1e300;
@@ -527,9 +530,9 @@ int32_t mux_decode_num_splits(int32_t num_seqs, int32_t hkv, int32_t head_dim, c
   for (int S : cands) {
     if (S > 1 && S > max_pages) break;
     const int64_t ctas = static_cast<int64_t>(num_seqs) * groups * S;
-    if (S > 1 && ctas > 16LL * num_sms) break;     // finer units cannot pay for themselves
+    if (S > 1 && ctas > 16LL * slots) break;       // finer units cannot pay for themselves
     const int C = (max_pages + S - 1) / S;
-    sm.assign(std::min<int64_t>(num_sms, ctas), 0.0);
+    sm.assign(std::min<int64_t>(slots, ctas), 0.0);
     std::priority_queue<double, std::vector<double>, std::greater<double>> q(sm.begin(), sm.end());
     double span = 0.0;
     for (int b = 0; b < num_seqs; ++b)
