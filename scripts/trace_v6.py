@@ -35,3 +35,10 @@ for h, (qk, s, mx, ex, pv) in enumerate([(8, 0, 2, 12, 6), (9, 1, 3, 13, 7)]):
           f"  P->PV issue {np.median((t[pv]-t[ex])[mid]):.0f}")
 print("B's S after A's S:", np.median((t[1] - t[0])[mid]), " A's QK(j+1) after B's S(j):",
       np.median((t[8, 1:nt] - t[1, :nt - 1])[mid]))
+# producer side: K(j) / V(j) TMA issue times (after their ring slot was released)
+kl, vl = t[10, :nt], t[11, :nt]
+if (kl > 0).all() and (vl > 0).all():
+  print("K(j) issued -> QK_A(j) issued", np.median((t[8, :nt] - kl)[mid]), " K(j) issued after QK_B(j-2) issued",
+      np.median((kl[2:] - t[9, :nt - 2])[mid]))
+  print("V(j) issued -> PV_A(j) issued", np.median((t[6, :nt] - vl)[mid]), " V(j) issued after PV_B(j-3) issued",
+      np.median((vl[3:] - t[7, :nt - 3])[mid]))
