@@ -241,6 +241,34 @@ def probe_read_bw(mux, part, wl, split, sms, nbytes=2 << 30, reps=3):
     return got * reps / (a.elapsed_time(b) * 1e-3) / 1e9
 
 
+def time_kernel_alone(mux, part, wl, split, which, reps=5):
+    """Average duration (s) of ONE attention launch (prefill6 / decode kernel of layer 0) on split
+    `split`'s own partition stream, nothing else running, CUDA events on that stream."""
+    import torch
+    _, _, sd, sp = part.query(split)
+    raw = sp if which == "pf" else sd
+    st = torch.cuda.ExternalStream(raw)
+    if which == "pf":
+        run = lambda: mux.mux_prefill_attn(wl.pool, 0, wl.pf_batch, wl.Hq, wl.pf_q, wl.pf_o, None,  # noqa: E731
+                                           scale=wl.scale, stream=raw)
+    else:
+        dsms = part.query(split)[0]
+        ns = mux.mux_decode_num_splits(wl.dc_spec.num_seqs, wl.Hkv, max(wl.dc_spec.L), dsms, wl.dc_spec.L, wl.d)
+        ws = torch.empty(max(16, mux.mux_decode_workspace_bytes(wl.dc_spec.num_seqs, wl.Hq, wl.d, ns)),
+                         dtype=torch.uint8, device="cuda")
+        run = lambda: mux.mux_decode_attn(wl.pool, 0, wl.dc_batch, wl.Hq, wl.dc_q, wl.dc_o, None,  # noqa: E731
+                                          scale=wl.scale, num_splits=ns, ws=ws, stream=raw)
+    torch.cuda.synchronize()
+    run()
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    a.record(st)
+    for _ in range(reps):
+        run()
+    b.record(st)
+    torch.cuda.synchronize()
+    return a.elapsed_time(b) / reps * 1e-3
+
+
 def time_side(mux, part, split, wl, which, iters, reps=3):
     """Isolated time (s) of one side on `split` (the other side NULL)."""
     import torch
@@ -538,17 +566,29 @@ def main():
         pass
     pf_share = best["pf_sms"] / total_sms
     dc_share = best["dec_sms"] / total_sms
+    # SURVEY §8(d) denominator (3): BW_read(k_d), a read-only 32 KiB bulk-copy stream (mux_stream_read)
+    # on the SAME decode partition, measured here (untimed region), alone and next to the prefill side
+    bw_part, bw_full = probe_read_bw(mux, part, wl, i, best["dec_sms"]), probe_read_bw(mux, part, wl, -1, total_sms)
+    # the dominant kernels alone on their own partitions (CUDA events on the partition stream)
+    t_pf_k = time_kernel_alone(mux, part, wl, i, "pf")
+    t_dc_k = time_kernel_alone(mux, part, wl, i, "dc")
     roofline = {"bound": "tensor", "kernel": "prefill side per layer: prefill6_kernel + outproj2_kernel (tcgen05)",
                 "achieved": pf_tflops,
                 "peak": tc_peak, "unit": "TFLOP/s", "frac": pf_tflops / tc_peak,
                 "frac_of_sm_share": pf_tflops / (tc_peak * pf_share), "peak_src": f"{peaks_src} bf16_tflops_sustained",
                 "traffic": (traffic.get("prefill6_kernel") or traffic.get("prefill_kernel") or {}).get("bytes"),
                 "traffic_kernel": "prefill6_kernel" if "prefill6_kernel" in traffic else "prefill_kernel",
+                "kernel_alone": {"kernel": "prefill6_kernel", "sms": best["pf_sms"], "launch_us": t_pf_k * 1e6,
+                                 "achieved": wl.prefill_flops_layer() / t_pf_k / 1e12,
+                                 "peak_burst_share": peaks["bf16_tflops"] * pf_share,
+                                 "frac_of_burst_share": wl.prefill_flops_layer() / t_pf_k / 1e12
+                                 / (peaks["bf16_tflops"] * pf_share),
+                                 "frac_of_sustained_share": wl.prefill_flops_layer() / t_pf_k / 1e12 / (tc_peak * pf_share),
+                                 "note": "5 launches of layer 0 on the prefill partition stream, nothing else running, "
+                                         "right after the timed steps (same power-capped clocks); peaks scaled by the "
+                                         "partition's SM share"},
                 "per_launch": (f"1 layer: causal prefill attention {wl.prefill_flops_layer():.3e} FLOP + o_proj "
                                f"{wl.pf_spec.total_new}x{wl.Hq * wl.d}x{wl.hidden} {wl.outproj_flops_layer(wl.pf_spec):.3e}")}
-    # SURVEY §8(d) denominator (3): BW_read(k_d), a read-only 32 KiB bulk-copy stream (mux_stream_read)
-    # on the SAME decode partition, measured here (untimed region), alone and next to the prefill side
-    bw_part, bw_full = probe_read_bw(mux, part, wl, i, best["dec_sms"]), probe_read_bw(mux, part, wl, -1, total_sms)
     roofline_dec = {"bound": "hbm", "kernel": "decode_kernel", "achieved": dc_gbs, "peak": peaks["hbm_gbs"],
                     "unit": "GB/s", "frac": dc_gbs / peaks["hbm_gbs"], "peak_src": f"{peaks_src} hbm_gbs",
                     "sm_share": dc_share, "partition_read_gbs": bw_part, "full_gpu_read_gbs": bw_full,
@@ -558,6 +598,9 @@ def main():
                     "iso_frac_of_partition_read": wl.decode_bytes_layer() / (best["t_dc_iso_ms"] * 1e-3 / wl.layers)
                     / 1e9 / bw_part,
                     "partition_read_src": f"mux_stream_read on the {best['dec_sms']}-SM decode partition (alone)",
+                    "kernel_alone": {"kernel": "decode_kernel (+ combine)", "sms": best["dec_sms"],
+                                     "launch_us": t_dc_k * 1e6, "achieved": wl.decode_bytes_layer() / t_dc_k / 1e9,
+                                     "frac_of_partition_read": wl.decode_bytes_layer() / t_dc_k / 1e9 / bw_part},
                     "traffic": traffic.get("decode_kernel", {}).get("bytes")}
     launches_per_step = wl.layers * 3 + wl.layers * iters * (3 + (1 if ns > 1 else 0)) + 4
     clocks = clk.summary()
