@@ -54,6 +54,19 @@ def _check(rc: int, what: str):
         raise RuntimeError(f"{what}: NCCL error {rc}: {lib().ncclGetErrorString(rc).decode()}")
 
 
+def uid_bytes(uid: _UniqueId) -> bytes:
+    """All 128 bytes of an ncclUniqueId (it is binary: `bytes(uid.internal)` would stop at the
+    first NUL, as ctypes reads c_char arrays as C strings, and hand other ranks a corrupt id)."""
+    return ctypes.string_at(ctypes.addressof(uid), ctypes.sizeof(_UniqueId))
+
+
+def uid_from_bytes(b: bytes) -> _UniqueId:
+    assert len(b) == ctypes.sizeof(_UniqueId), len(b)
+    uid = _UniqueId()
+    ctypes.memmove(ctypes.addressof(uid), b, len(b))
+    return uid
+
+
 class Comm:
     """A NCCL communicator over all ranks of the default torch.distributed group."""
 
@@ -63,9 +76,9 @@ class Comm:
         if rank == 0:
             _check(lib().ncclGetUniqueId(ctypes.byref(uid)), "ncclGetUniqueId")
         if world > 1:
-            obj = [bytes(uid.internal) if rank == 0 else None]
+            obj = [uid_bytes(uid) if rank == 0 else None]
             dist.broadcast_object_list(obj, src=0)
-            ctypes.memmove(ctypes.addressof(uid), obj[0], 128)
+            uid = uid_from_bytes(obj[0])
         self.comm = ctypes.c_void_p()
         _check(lib().ncclCommInitRank(ctypes.byref(self.comm), world, uid, rank), "ncclCommInitRank")
 

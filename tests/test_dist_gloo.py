@@ -82,3 +82,37 @@ def test_shard_ranges():
     with pytest.raises(ValueError):
         shard.kv_head_range(0, 3, 8)
     assert shard.page_table_hash([0, 2], [5, 7]) != shard.page_table_hash([0, 2], [7, 5])
+
+
+def _uid_worker(rank, world, port, q):
+    import torch.distributed as dist
+    from paper_2504_14489_b200 import nccl
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        raw = bytes([(7 * i) % 5 for i in range(128)])      # binary, NULs at every 5th byte
+        uid = nccl.uid_from_bytes(raw) if rank == 0 else nccl._UniqueId()
+        obj = [nccl.uid_bytes(uid) if rank == 0 else None]  # the exchange nccl.Comm performs
+        dist.broadcast_object_list(obj, src=0)
+        got = nccl.uid_bytes(nccl.uid_from_bytes(obj[0]))
+        res = [None] * world
+        dist.all_gather_object(res, got == raw)
+        if rank == 0:
+            q.put(res)
+    finally:
+        dist.destroy_process_group()
+
+
+def test_nccl_unique_id_broadcast_keeps_binary_bytes():
+    """nccl.Comm hands rank 0's ncclUniqueId to the other ranks through torch.distributed; the id
+    is binary, so the bytes must survive embedded NULs (world 2, gloo)."""
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    ps = [ctx.Process(target=_uid_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in ps:
+        p.start()
+    res = q.get(timeout=120)
+    for p in ps:
+        p.join(timeout=60)
+    assert res == [True, True]
