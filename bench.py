@@ -560,7 +560,7 @@ def main():
     tc_peak = peaks.get("bf16_tflops_sustained", peaks["bf16_tflops"])
     traffic = {}
     try:
-        with open(os.path.join(ROOT, "profiles", "r01s2_traffic.json")) as f:
+        with open(os.path.join(ROOT, "profiles", "r01s3_traffic.json")) as f:
             traffic = json.load(f)
     except Exception:
         pass
