@@ -241,6 +241,26 @@ def probe_read_bw(mux, part, wl, split, sms, nbytes=2 << 30, reps=3):
     return got * reps / (a.elapsed_time(b) * 1e-3) / 1e9
 
 
+def probe_read_bw_contended(mux, part, wl, split, sms, pf_side, nbytes=2 << 30, reps=6):
+    """BW_read(k) with the prefill side running: the same probe on split `split`'s decode stream
+    while mux_run_layer runs the step's prefill side (32 layers, ~30 ms) on the prefill partition,
+    i.e. the decode partition's read bandwidth under the mux step's HBM/L2/power contention."""
+    import torch
+    st = torch.cuda.ExternalStream(part.query(split)[2])
+    src = wl.kpool.view(-1)
+    nb = min(nbytes, src.numel() * src.element_size())
+    torch.cuda.synchronize()
+    mux.mux_run_layer(part, split, wl.pool, pf_side, None)     # asynchronous: prefill partition busy
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    mux.mux_stream_read(src, sms, st, nb)                       # warm, inside the prefill window
+    a.record(st)
+    for _ in range(reps):
+        got = mux.mux_stream_read(src, sms, st, nb)
+    b.record(st)
+    torch.cuda.synchronize()
+    return got * reps / (a.elapsed_time(b) * 1e-3) / 1e9
+
+
 def time_kernel_alone(mux, part, wl, split, which, reps=5):
     """Average duration (s) of ONE attention launch (prefill6 / decode kernel of layer 0) on split
     `split`'s own partition stream, nothing else running, CUDA events on that stream."""
@@ -569,6 +589,7 @@ def main():
     # SURVEY §8(d) denominator (3): BW_read(k_d), a read-only 32 KiB bulk-copy stream (mux_stream_read)
     # on the SAME decode partition, measured here (untimed region), alone and next to the prefill side
     bw_part, bw_full = probe_read_bw(mux, part, wl, i, best["dec_sms"]), probe_read_bw(mux, part, wl, -1, total_sms)
+    bw_part_mux = probe_read_bw_contended(mux, part, wl, i, best["dec_sms"], pf)
     # the dominant kernels alone on their own partitions (CUDA events on the partition stream)
     t_pf_k = time_kernel_alone(mux, part, wl, i, "pf")
     t_dc_k = time_kernel_alone(mux, part, wl, i, "dc")
@@ -598,6 +619,10 @@ def main():
                     "iso_frac_of_partition_read": wl.decode_bytes_layer() / (best["t_dc_iso_ms"] * 1e-3 / wl.layers)
                     / 1e9 / bw_part,
                     "partition_read_src": f"mux_stream_read on the {best['dec_sms']}-SM decode partition (alone)",
+                    "partition_read_gbs_contended": bw_part_mux,
+                    "frac_of_partition_read_contended": dc_gbs / bw_part_mux,
+                    "partition_read_contended_src": "the same probe while the step's prefill side runs on the "
+                                                    "prefill partition (same run, same clocks regime)",
                     "kernel_alone": {"kernel": "decode_kernel (+ combine)", "sms": best["dec_sms"],
                                      "launch_us": t_dc_k * 1e6, "achieved": wl.decode_bytes_layer() / t_dc_k / 1e9,
                                      "frac_of_partition_read": wl.decode_bytes_layer() / t_dc_k / 1e9 / bw_part},
