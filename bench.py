@@ -492,12 +492,16 @@ def main():
     with ClockSampler(local) as clk:
         torch.cuda.synchronize()
         a.record(st)
+        step_ev = []
         for _ in range(args.steps):
             mux.mux_run_layer(part, i, wl.pool, pf, dc, times)
+            step_ev.append(torch.cuda.Event(enable_timing=True))
+            step_ev[-1].record(st)
         b.record(st)
         torch.cuda.synchronize()
     tt = times.cpu().numpy()
     t_step = a.elapsed_time(b) / args.steps * 1e-3
+    step_ms = [a.elapsed_time(step_ev[0])] + [step_ev[k - 1].elapsed_time(step_ev[k]) for k in range(1, len(step_ev))]
     if world > 1:
         tm = torch.tensor([t_step], device="cuda", dtype=torch.float64)
         dist.all_reduce(tm, op=dist.ReduceOp.MAX)
@@ -641,6 +645,7 @@ def main():
         "roofline": roofline, "roofline_decode": roofline_dec,
         "e2e": {"value": toks / t_e2e, "unit": "tok/s", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h},
         "gpu_launches": launches_per_step * args.steps,
+        "step_ms_p10_p50_p90": [float(np.percentile(step_ms, q)) for q in (10, 50, 90)],
         "clocks": clocks,
         "iso_full_gpu_ms": {"prefill_32_layers": full_pf * 1e3, "decode_iter_32_layers": full_dc * 1e3},
         "time_sliced_tok_s": (wl.pf_spec.total_new + wl.dc_spec.num_seqs * iters) / (full_pf + iters * full_dc),
