@@ -49,7 +49,10 @@ template <int NT> struct DecodeCfg {
   static constexpr int kCtasPerSm = MUX_DEC_2CTA ? 2 : 1;
   static constexpr int kThreads = (kConsumerWarps + 2) * 32;   // + K producer + V producer
 };
-constexpr int kRingBytes = (MUX_DEC_2CTA ? 96 : 192) * 1024;   // K and V page stages in flight per CTA
+#ifndef MUX_DEC_RING_KB
+#define MUX_DEC_RING_KB 192   // A/B switch: KiB of K + V stages per CTA (1 CTA / SM)
+#endif
+constexpr int kRingBytes = (MUX_DEC_2CTA ? MUX_DEC_RING_KB / 2 : MUX_DEC_RING_KB) * 1024;   // K and V stages in flight per CTA
 
 struct DecodeParams {
   const uint16_t* q;         // [B][Hq][D]
