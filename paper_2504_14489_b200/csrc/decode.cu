@@ -6,8 +6,8 @@
 // exact reorganisation of the softmax.
 //
 // B200 design: HBM-bound, so the kernel is a page-streaming engine.
-//   grid (num_splits, Hkv/HG, B); one CTA per SM; 9 warps: warp 8 = producer, 0-7 consumers.
-//   Producer: one lane issues TWO TMA ops per page (cp.async.bulk.tensor.5d, SWIZZLE_128B):
+//   grid (num_splits, Hkv/HG, B); one CTA per SM; 10 warps: 0-7 consumers, 8 K producer, 9 V producer.
+//   Producers: one lane each issues one TMA op per page (cp.async.bulk.tensor.5d, SWIZZLE_128B):
 //   the K and the V block of the page for all HG (<= 8) kv heads of the CTA's group — 32 KiB
 //   each at d=128, HG=8.  The per-SM TMA engine is op-rate bound (measured: 2 KiB boxes cap
 //   an SM at ~49 GB/s, 32 KiB ops at ~200 GB/s), so big boxes are what lets a 16-48 SM
@@ -15,12 +15,17 @@
 //   Consumers: warp w owns kv head w%HG and every (8/HG)-th page; legacy tensor pipe (the
 //   group of g <= 8 q heads is the N=8 side, so FP32 ALU is left for the softmax):
 //     S^T[16 tok x 8 heads] = K_page[16 x d] . Q^T      (mma.m16n8k16, A = K via ldmatrix)
-//     online softmax per head column (warp shuffles over the 8 token lanes)
+//     online softmax per head column with a lazy reference max (moves only when a score exceeds it
+//     by > 8); the exact page max (warp shuffles over the 8 token lanes) only when a warp vote
+//     says some column grew
 //     P^T -> B fragments with movmatrix.trans (no smem round trip), P = P_hi + P_lo in
 //     two bf16 halves (~16-bit P)
 //     O^T[d x 8] += V_page^T . P_hi^T + V_page^T . P_lo^T (A = V^T via ldmatrix.trans)
 //   Warps merge their (m, l, O) states in smem at the end; with one split the CTA writes
 //   the normalised output, otherwise fp32 partials (o, m, l) for the combine kernel.
+//   Per SM the kernel is bound by the shared-memory port (TMA writes + ldmatrix reads of every KV
+//   byte, 128 B/clk) and the per-page dependency chain; the A/B switches below (MUX_DEC_*) record the
+//   variants measured against it (profiles/r01_summary.md).
 #include <math.h>
 
 #include <algorithm>
