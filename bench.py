@@ -438,10 +438,11 @@ def main():
         dsms, psms, _, _ = part.query(i)
         t_dc = time_side(mux, part, i, wl, "dc", 1)          # one decode iteration (N_T layers)
         t_pf = time_side(mux, part, i, wl, "pf", 1)          # the whole prefill (N_T layers)
-        # decode iterations per whole prefill = N_T / N_PL; both neighbours of the ratio are
-        # measured below and the faster kept (a plain round() flips with timing noise near .5)
+        # decode iterations per whole prefill = N_T / N_PL from the isolated times; both
+        # neighbours of the ratio, and one fewer (contention slows the decode side more than the
+        # prefill side in the mux window), are measured below and the fastest kept
         r = t_pf / t_dc
-        for iters in sorted({max(1, math.floor(r)), max(1, math.ceil(r))}):
+        for iters in sorted({max(1, math.floor(r) - 1), max(1, math.floor(r)), max(1, math.ceil(r))}):
             sweep.append({"split": i, "dec_sms": dsms, "pf_sms": psms, "t_dc_iso_ms": t_dc * 1e3,
                           "t_pf_iso_ms": t_pf * 1e3, "iters": iters})
 
