@@ -311,6 +311,20 @@ typedef struct {
   int32_t keep_pages;           /* 1: finished requests keep their pages (for inspection) */
   int32_t serialize;            /* 1: temporal multiplexing baseline: both sides on ONE whole-GPU
                                    stream (no overlap); fixed_split must be -1 */
+  /* f2 launch-gap removal ("each decode iteration as a CUDA graph"): 1 = every decode
+   * iteration (gathers + N_T x (append, attention, combine, out-projection)) is ONE graph launch,
+   * captured lazily per (split, batch size, split-KV count, pages per split) and replayed; the
+   * iteration's batch arrays are copied into a fixed device buffer right before the launch. */
+  int32_t use_graphs;
+  /* Output log (optional, for checking the engine's results): after every decode iteration and
+   * after the last layer group of every prefill batch, the LAST layer's attention output rows
+   * (o_f32 ? f32 : bf16, [rows][Hq][d]) are appended to o_log and, with w_o, the out-projection
+   * rows (bf16 [rows][hidden]) to y_log, until log_rows rows are used (device buffers, owned by
+   * the caller).  mux_engine_out_rows() says which (request, position) each row holds. */
+  void* o_log;
+  void* y_log;
+  int32_t log_rows;
+  int32_t o_f32;                /* 1: attention outputs in f32 (needs w_o == NULL); 0: bf16 */
 } mux_engine_desc;
 
 typedef struct {
@@ -319,6 +333,12 @@ typedef struct {
   int32_t prompt;               /* n >= 1: new prompt tokens (prefill) */
   int32_t gen;                  /* decode iterations after the prefill (>= 0) */
   int32_t src_base;
+  /* arrival (online serving): the request joins the FCFS queue once the engine has COMPLETED
+   * arrival_iter decode iterations AND arrival_us microseconds (host clock) have passed since
+   * mux_engine_run started; 0 / 0 = at the start.  A request whose arrival_iter cannot be reached
+   * (no decode work left) is admitted when the engine would otherwise idle. */
+  int32_t arrival_iter;
+  double arrival_us;
 } mux_request;
 
 typedef struct {
@@ -329,11 +349,17 @@ typedef struct {
   double bubble_ratio;          /* R21: idle share of each side's [first, last] window, averaged */
   double bubble_ratio_dec, bubble_ratio_pf;
   double tbt_mean_us, tbt_max_us; /* decode iteration end-to-end intervals */
-  double ttft_mean_us, ttft_max_us;
+  double ttft_mean_us, ttft_max_us;   /* prefill completion - arrival, device clock */
+  /* launch gap (f2): device idle time of the decode side between consecutive decode iterations
+   * (start of iteration i+1 - end of iteration i, %globaltimer), i.e. the host's turn-around */
+  double gap_mean_us, gap_max_us;
+  int32_t graphs;               /* CUDA graphs captured (use_graphs) */
+  int64_t graph_bytes;          /* device memory taken by instantiating them (cudaMemGetInfo delta) */
+  int32_t logged_rows;          /* rows written to o_log / y_log */
 } mux_engine_stats;
 
 int mux_engine_create(mux_engine_t* out, mux_part_t part, mux_pool_t pool, const mux_engine_desc* desc);
-/* queue requests (FCFS); all are considered to arrive at the start of mux_engine_run */
+/* queue requests (FCFS in arrival order, submission order among equal arrivals) */
 int mux_engine_submit(mux_engine_t eng, const mux_request* reqs, int32_t n);
 /* run until every submitted request has finished its decode; blocks the calling thread */
 int mux_engine_run(mux_engine_t eng, mux_engine_stats* stats);
@@ -342,6 +368,10 @@ int mux_engine_request_pages(mux_engine_t eng, int32_t id, int32_t* kv_len, int3
                              int32_t* n_pages);
 /* per-iteration trace: for decode iteration i, out[i] = {split, batch size, start, end (ns)} */
 int mux_engine_trace(mux_engine_t eng, int64_t* out, int32_t cap, int32_t* n);
+/* the output log's rows (after mux_engine_run): out[3*i] = request id, out[3*i+1] = absolute
+ * position p of the query token (it attended keys 0..p of the request), out[3*i+2] = 0 for a
+ * prefill row, 1 for a decode row; row i of o_log / y_log.  *n = rows logged. */
+int mux_engine_out_rows(mux_engine_t eng, int32_t* out, int32_t cap, int32_t* n);
 int mux_engine_destroy(mux_engine_t eng);
 
 /* ------------------------------------------------------------------------------------

@@ -16,15 +16,30 @@ FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std
          "--expt-relaxed-constexpr", "-Xcompiler", "-fPIC,-fvisibility=hidden", "-Xptxas", "-v",
          "-I", os.path.join(ROOT, "include")]
 # developer A/B builds only (e.g. MUX_NVCC_EXTRA="-DMUX_EMU_PAIRS=0x1111u"); empty in production
-FLAGS += os.environ.get("MUX_NVCC_EXTRA", "").split()
+EXTRA = os.environ.get("MUX_NVCC_EXTRA", "").split()
+FLAGS += EXTRA
+# recorded in mux_version() (common.cu) so every consumer can see which build it loaded
+FLAGS += ["-DMUX_EXTRA_FLAGS=\"" + " ".join(EXTRA).replace('"', "") + "\""]
+STAMP = SO + ".flags"
 
 
 def sources():
     return sorted(glob.glob(os.path.join(CSRC, "*.cu")))
 
 
+def _stamp_text() -> str:
+    return " ".join([NVCC] + FLAGS)
+
+
 def needs_build() -> bool:
     if not os.path.exists(SO):
+        return True
+    # a build with other flags (e.g. an A/B define left in libmux.so) is rebuilt, not reused
+    try:
+        with open(STAMP) as f:
+            if f.read() != _stamp_text():
+                return True
+    except OSError:
         return True
     t = os.path.getmtime(SO)
     deps = sources() + glob.glob(os.path.join(CSRC, "*.h")) + [os.path.join(ROOT, "include", "mux.h")]
@@ -52,6 +67,8 @@ def build(force: bool = False, verbose: bool = False) -> str:
     if r.returncode != 0:
         sys.stderr.write(r.stdout + r.stderr)
         raise RuntimeError("link failed")
+    with open(STAMP, "w") as f:
+        f.write(_stamp_text())
     return SO
 
 

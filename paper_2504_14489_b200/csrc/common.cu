@@ -130,7 +130,12 @@ extern "C" {
 
 const char* mux_last_error(void) { return mux::g_last_error.c_str(); }
 
-const char* mux_version(void) { return "mux-b200 0.1 sm_100a"; }
+#ifndef MUX_EXTRA_FLAGS
+#define MUX_EXTRA_FLAGS ""
+#endif
+// the developer A/B defines this build was compiled with (build.py passes MUX_NVCC_EXTRA here), so a
+// bench line or test log can tell a production build ("extra=") from an A/B build
+const char* mux_version(void) { return "mux-b200 0.2 sm_100a extra=" MUX_EXTRA_FLAGS; }
 
 int32_t mux_partition_configs(int32_t total_sms, int32_t granularity, int32_t min_side, int32_t* out,
                               int32_t cap) {

@@ -485,7 +485,7 @@ int launch_decode(mux_pool* pool, const DecodeParams& prm, int B, cudaStream_t s
     case 4: return launch_decode_hg<D, NT, 4>(pool, prm, B, st);
     case 2: return launch_decode_hg<D, NT, 2>(pool, prm, B, st);
     case 1: return launch_decode_hg<D, NT, 1>(pool, prm, B, st);
-    default: return fail(MUX_ERR_UNSUPPORTED, "Hkv must be a multiple of 1, 2, 4 or 8");
+    default: return fail(MUX_ERR_UNSUPPORTED, "internal: kv heads per decode CTA not in {1, 2, 4, 8}");
   }
 }
 
@@ -507,8 +507,8 @@ int32_t mux_decode_num_splits(int32_t num_seqs, int32_t hkv, int32_t head_dim, c
   if (num_seqs < 1 || hkv < 1 || max_kv < 1) return 1;
   if (num_sms < 1) num_sms = 148;
   if (head_dim < 1) head_dim = 128;
-  int hg = 1;
-  for (int c = 1; c <= (MUX_DEC_2CTA ? 4 : 8); ++c)
+  int hg = 1;   // as pool_tmaps: the largest power of two <= 8 dividing Hkv
+  for (int c = 2; c <= (MUX_DEC_2CTA ? 4 : 8); c *= 2)
     if (hkv % c == 0) hg = c;
   const int groups = hkv / hg;
   const int max_pages = (max_kv + kPage - 1) / kPage;

@@ -15,11 +15,18 @@
 // staged in pinned memory and copied with the iteration on its own stream; activations are
 // gathered from the caller's synthetic source rows by a copy kernel.  Every iteration and
 // group is bracketed by %globaltimer stamps in a device log, from which the run's bubble
-// ratio, TBT and TTFT are computed after the run (no profiler, no host clocks).
+// ratio, TBT, TTFT and the decode side's inter-iteration launch gap are computed after the run
+// (no profiler).  f2 launch-gap removal: with use_graphs every decode iteration is
+// ONE CUDA graph launch (captured lazily per (split, batch size, split-KV count, pages per split),
+// replayed with the batch arrays copied into a fixed device buffer first).  Requests arrive over
+// time (arrival_iter / arrival_us): prefills then merge into a RUNNING decode batch.
 #include <algorithm>
+#include <chrono>
 #include <cmath>
 #include <deque>
+#include <map>
 #include <thread>
+#include <tuple>
 #include <vector>
 
 #include "pool.h"
@@ -53,6 +60,8 @@ struct Req {
   int ctx = 0;          // tokens in the pool (kv_len after the last append)
   int gen_left = 0;
   int ttft_log = -1;    // log slot of the end stamp of its last prefill group
+  int arrive_log = -1;  // log slot of the end stamp of the decode iteration that met arrival_iter
+  bool arrived = false;
   bool finished = false;
 };
 
@@ -92,9 +101,16 @@ struct mux_engine {
   std::vector<double> dec_theta, pf_theta, slowdown;
   std::vector<mux::Req> reqs;
   int Hkv = 0, d = 0, NT = 0;
+  size_t osz = 2;                      // bytes per attention output element (bf16 / f32)
   // device buffers
   void *dq = nullptr, *dk = nullptr, *dv = nullptr, *do_ = nullptr, *dy = nullptr, *ws = nullptr;
+  int32_t* dfix = nullptr;             // the decode iteration's batch arrays (fixed address: graphs)
   size_t ws_bytes = 0;
+  // f2: decode-iteration graphs keyed by (split, batch size, split-KV count, pages per split)
+  std::map<std::tuple<int, int, int, int>, cudaGraphExec_t> graphs;
+  int64_t graph_bytes = 0;
+  std::vector<int32_t> out_rows;       // [row][3] = request id, position, decode?
+  int log_rows_used = 0;
   void *pq[2] = {}, *pk[2] = {}, *pv[2] = {}, *po[2] = {}, *py[2] = {};
   void *prek = nullptr, *prev = nullptr;
   int cap_dec = 0, cap_pf = 0, cap_pre = 0;
@@ -136,6 +152,16 @@ int new_event(mux_engine* e, cudaEvent_t* ev) {
   return MUX_OK;
 }
 
+int event_done(cudaEvent_t ev, bool* done) {
+  const cudaError_t q = cudaEventQuery(ev);
+  *done = q == cudaSuccess;
+  if (q == cudaSuccess || q == cudaErrorNotReady) {
+    if (q == cudaErrorNotReady) cudaGetLastError();   // not an error: clear it
+    return MUX_OK;
+  }
+  return cuda_fail(q, "engine: cudaEventQuery (a kernel of the run failed)");
+}
+
 int log_pair(mux_engine* e, int* idx) {
   if (e->log_n + 2 > e->log_cap) return fail(MUX_ERR_INVALID_ARG, "engine log full");
   *idx = e->log_n;
@@ -162,6 +188,9 @@ int mux_engine_create(mux_engine_t* out, mux_part_t part, mux_pool_t pool, const
   if (desc->serialize && desc->fixed_split != -1) return fail(MUX_ERR_INVALID_ARG, "serialize needs fixed_split = -1");
   if (desc->fixed_split == -2 && (!model || desc->n_cost != nsplit))
     return fail(MUX_ERR_INVALID_ARG, "best-fit split needs a cost model with one entry per split");
+  if (desc->o_f32 && desc->w_o) return fail(MUX_ERR_INVALID_ARG, "o_f32 needs w_o == NULL (the out-projection reads bf16 O)");
+  if (desc->log_rows < 0 || (desc->log_rows > 0 && !desc->o_log) || (desc->log_rows > 0 && desc->w_o && !desc->y_log))
+    return fail(MUX_ERR_INVALID_ARG, "output log: o_log (and y_log with w_o) needed for log_rows > 0");
   auto* e = new mux_engine();
   e->part = part;
   e->pool = pool;
@@ -169,6 +198,7 @@ int mux_engine_create(mux_engine_t* out, mux_part_t part, mux_pool_t pool, const
   e->Hkv = Hkv;
   e->d = d;
   e->NT = pool->desc.num_layers;
+  e->osz = desc->o_f32 ? 4 : 2;
   if (model) {
     e->dec_theta.assign(desc->dec_theta, desc->dec_theta + 3 * desc->n_cost);
     e->pf_theta.assign(desc->pf_theta, desc->pf_theta + 4 * desc->n_cost);
@@ -186,6 +216,7 @@ int mux_engine_submit(mux_engine_t e, const mux_request* rq, int32_t n) {
     if (rq[i].prompt < 1 || rq[i].cached < 0 || rq[i].gen < 0)
       return fail(MUX_ERR_INVALID_ARG, "request needs prompt >= 1, cached >= 0, gen >= 0");
     if (rq[i].prompt > e->desc.max_prefill_tokens) return fail(MUX_ERR_INVALID_ARG, "prompt > max_prefill_tokens");
+    if (rq[i].arrival_iter < 0 || !(rq[i].arrival_us >= 0.0)) return fail(MUX_ERR_INVALID_ARG, "arrival must be >= 0");
     Req r;
     r.r = rq[i];
     e->reqs.push_back(r);
@@ -208,7 +239,8 @@ static int engine_alloc(mux_engine* e) {
   MUX_CUDA(cudaMalloc(&e->dq, e->cap_dec * qrow));
   MUX_CUDA(cudaMalloc(&e->dk, e->cap_dec * kvrow));
   MUX_CUDA(cudaMalloc(&e->dv, e->cap_dec * kvrow));
-  MUX_CUDA(cudaMalloc(&e->do_, e->cap_dec * qrow));
+  const size_t orow = static_cast<size_t>(Hq) * d * e->osz;
+  MUX_CUDA(cudaMalloc(&e->do_, e->cap_dec * orow));
   if (e->desc.w_o) MUX_CUDA(cudaMalloc(&e->dy, static_cast<size_t>(e->cap_dec) * e->desc.hidden * 2));
   e->ws_bytes = mux_decode_workspace_bytes(e->cap_dec, Hq, d, 64);
   MUX_CUDA(cudaMalloc(&e->ws, std::max<size_t>(e->ws_bytes, 256)));
@@ -216,7 +248,7 @@ static int engine_alloc(mux_engine* e) {
     MUX_CUDA(cudaMalloc(&e->pq[i], e->cap_pf * qrow));
     MUX_CUDA(cudaMalloc(&e->pk[i], e->cap_pf * kvrow));
     MUX_CUDA(cudaMalloc(&e->pv[i], e->cap_pf * kvrow));
-    MUX_CUDA(cudaMalloc(&e->po[i], e->cap_pf * qrow));
+    MUX_CUDA(cudaMalloc(&e->po[i], e->cap_pf * orow));
     if (e->desc.w_o) MUX_CUDA(cudaMalloc(&e->py[i], static_cast<size_t>(e->cap_pf) * e->desc.hidden * 2));
   }
   MUX_CUDA(cudaMalloc(&e->prek, e->cap_pre * kvrow));
@@ -228,9 +260,10 @@ static int engine_alloc(mux_engine* e) {
     if (!rc) rc = slot_reserve(e->preslot[i], 4 * nreq + 8 + tot_pages + e->cap_pre);
     if (rc) return rc;
   }
+  MUX_CUDA(cudaMalloc(&e->dfix, (4 * static_cast<size_t>(e->cap_dec) + 8 + tot_pages) * 4));
   e->log_cap = static_cast<int>(2 * (iters + static_cast<int64_t>(e->NT) * nreq + 64));
   MUX_CUDA(cudaMalloc(&e->log, static_cast<size_t>(e->log_cap) * 8));
-  return MUX_OK;
+  return pool_tmaps(e->pool);   // device-side pool state exists before any graph capture
 }
 
 // host arrays of a batch in a slot: [qo (B+1)][kv (B)][pind (B+1)][idx rows][page ids]
@@ -242,7 +275,9 @@ struct Built {
 };
 
 static Built build_batch(Slot& s, const std::vector<Req*>& rs, const std::vector<int>& n_new,
-                         const std::vector<int>& kv, const std::vector<int>& pos0, int src_rows) {
+                         const std::vector<int>& kv, const std::vector<int>& pos0, int src_rows,
+                         int32_t* dev = nullptr /* device copy of the arrays: default the slot's */) {
+  if (!dev) dev = s.d;
   Built out;
   const int B = static_cast<int>(rs.size());
   int32_t* qo = s.h;
@@ -268,10 +303,10 @@ static Built build_batch(Slot& s, const std::vector<Req*>& rs, const std::vector
   out.n = static_cast<size_t>(pids + pg - s.h);
   mux_batch& b = out.b;
   b.num_seqs = B;
-  b.qo_indptr = s.d;
-  b.kv_len = s.d + B + 1;
-  b.page_indptr = s.d + 2 * B + 1;
-  b.page_ids = s.d + 3 * B + 2 + rows;
+  b.qo_indptr = dev;
+  b.kv_len = dev + B + 1;
+  b.page_indptr = dev + 2 * B + 1;
+  b.page_ids = dev + 3 * B + 2 + rows;
   b.total_q = rows;
   b.max_q = max_q;
   b.max_kv = max_kv;
@@ -279,7 +314,7 @@ static Built build_batch(Slot& s, const std::vector<Req*>& rs, const std::vector
   b.h_kv_len = kl;
   b.h_page_indptr = pi;
   b.h_page_ids = pids;
-  out.d_idx = s.d + 3 * B + 2;
+  out.d_idx = dev + 3 * B + 2;
   out.rows = rows;
   return out;
 }
@@ -351,10 +386,14 @@ int mux_engine_run(mux_engine_t e, mux_engine_stats* st) {
     return best >= 0 ? best : big;  // infeasible SLO: the largest decode share
   };
 
+  bool done = false;
   while (true) {
     bool did = false;
     // ---- 1. decode iteration completed: tokens "returned", finished requests retire
-    if (dec_inflight && cudaEventQuery(dec_ev) == cudaSuccess) {
+    // event_done: cudaSuccess -> true, cudaErrorNotReady -> false, anything else (a sticky fault of
+    // a kernel, e.g. cudaErrorIllegalAddress) ends the run with MUX_ERR_CUDA instead of polling forever
+    if (dec_inflight && (rc = event_done(dec_ev, &done)) != MUX_OK) return rc;
+    if (dec_inflight && done) {
       dec_inflight = false;
       did = true;
       std::vector<int> keep;
@@ -366,7 +405,9 @@ int mux_engine_run(mux_engine_t e, mux_engine_stats* st) {
       decode = keep;
     }
     // ---- 2. prefill groups completed (in order); a finished prefill is ready to merge
-    while (!pf_out.empty() && cudaEventQuery(pf_out.front().ev) == cudaSuccess) {
+    while (!pf_out.empty()) {
+      if ((rc = event_done(pf_out.front().ev, &done)) != MUX_OK) return rc;
+      if (!done) break;
       Group g = pf_out.front();
       pf_out.pop_front();
       did = true;

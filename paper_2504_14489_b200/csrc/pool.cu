@@ -30,8 +30,10 @@ int pool_tmaps(mux_pool* p) {
 #ifndef MUX_DEC_2CTA
 #define MUX_DEC_2CTA 0
 #endif
+  // kv heads per decode CTA (csrc/decode.cu): the largest power of two <= 8 (4 under the 2-CTA
+  // switch) dividing Hkv, the instantiations launch_decode has (Hkv = 3, 6, 12 ... -> 1 or 2)
   int hg = 1;
-  for (int c = 1; c <= (MUX_DEC_2CTA ? 4 : 8); ++c)   // kv heads per decode CTA (csrc/decode.cu)
+  for (int c = 2; c <= (MUX_DEC_2CTA ? 4 : 8); c *= 2)
     if (d.num_kv_heads % c == 0) hg = c;
   p->hg = hg;
   uint32_t box1[5] = {64, static_cast<uint32_t>(kPage), static_cast<uint32_t>(D / 64), 1, 1};

@@ -16,7 +16,7 @@ struct mux_pool {
   // tmap_*g: box = one page of a whole kv-head group of hg heads (hg x 4 KiB)        -> decode
   // tmap_kh: box = one 64-dim half of one (page, kv head) block (2 KiB)            -> prefill K
   CUtensorMap tmap_k1, tmap_v1, tmap_kg, tmap_vg, tmap_kh;
-  int hg = 1;                        // kv heads per decode CTA (largest divisor of Hkv <= 8)
+  int hg = 1;                        // kv heads per decode CTA (largest power of two <= 8 dividing Hkv)
   int* d_err = nullptr;              // device error word (bit 0: prefill clamped a V value to fp16 range)
   int64_t layer_elems() const {      // elements per layer of K (or V)
     return static_cast<int64_t>(desc.num_pages) * desc.num_kv_heads * mux::kPage * desc.head_dim;

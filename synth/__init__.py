@@ -205,3 +205,23 @@ def sample_rows(total: int, k: int, tile: int = 128, extra: Optional[List[int]] 
     spread = np.linspace(0, total - 1, num=max(2, k - len(rows))).astype(np.int64)
     rows.update(int(x) for x in spread)
     return np.array(sorted(r for r in rows if 0 <= r < total), dtype=np.int32)
+
+
+def sample_rows_tiles(total: int, k: int, tile: int = 128) -> np.ndarray:
+    """Parity sample of about k rows spread over ALL q tiles (the late, heavy tiles of
+    a causal prefill must be sampled as densely as the early ones): first and last row; the first
+    and last row of the last 4 tiles and of evenly spaced tiles across the whole range; the rest
+    uniform.  Sorted, unique."""
+    nt = (total + tile - 1) // tile
+    rows = {0, total - 1}
+    picks = set(range(max(0, nt - 4), nt)) | {int(x) for x in np.linspace(0, nt - 1, num=min(nt, max(1, k // 8)))}
+    for t in sorted(picks):
+        rows.update({t * tile, min(total - 1, t * tile + tile - 1)})
+    extra = max(2, k - len(rows))
+    while True:
+        spread = np.linspace(0, total - 1, num=min(total, extra)).astype(np.int64)
+        got = rows | {int(x) for x in spread}
+        if len(got) >= min(k, total) or extra >= total:
+            break
+        extra += min(k, total) - len(got)
+    return np.array(sorted(r for r in got if 0 <= r < total), dtype=np.int32)

@@ -92,13 +92,19 @@ def gpu_build_side(mux, side: SideData, num_pages: int, seed: int, Hkv: int, d: 
                 page_ids=np.array(pids, np.int32), kv_len=np.array(L, np.int32), qo_indptr=indptr(spec.n))
 
 
-def check_close(gpu_out, ref, atol=2e-3, rtol=1e-2, what=""):
-    """DESIGN.md R8: BASELINE's "max-abs 2e-3 and relative 1e-2" read as the element-wise
-    allclose bound |d| <= atol + rtol*|ref| (fp32 and bf16 outputs alike)."""
+def check_close(gpu_out, ref, atol=2e-3, rtol=1e-2, what="", out_bf16=False):
+    """DESIGN.md R8, BASELINE's "max-abs 2e-3 and relative 1e-2":
+      * fp32 outputs (out_bf16=False): max|d| <= atol  AND  |d| <= atol + rtol*|ref| element-wise;
+      * bf16 outputs (out_bf16=True): the element-wise form only, because the bf16 rounding of the
+        output alone is up to 2^-9 |O| (3.9e-3 for |O| in [1, 2)), more than atol.
+    Returns the max |d|."""
     g = np.asarray(gpu_out, dtype=np.float64)
     diff = np.abs(g - ref)
-    bad = diff > atol + rtol * np.abs(ref)
     assert not np.isnan(g).any(), f"{what}: NaN in GPU output"
+    if not out_bf16:
+        assert diff.max() <= atol, (f"{what}: max|d|={diff.max():.3e} > {atol:.1e} at "
+                                    f"{np.unravel_index(diff.argmax(), diff.shape)}")
+    bad = diff > atol + rtol * np.abs(ref)
     assert not bad.any(), (f"{what}: {bad.sum()} elements out of tolerance; max|d|={diff.max():.3e} "
                            f"at {np.unravel_index(diff.argmax(), diff.shape)}")
     return float(diff.max())

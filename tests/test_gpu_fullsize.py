@@ -108,21 +108,36 @@ def test_fullsize_sampled_parity(mux, part, cfg, split):
     mux.mux_run_layer(part, split, pool, s_pf, s_dc, None)
     torch.cuda.synchronize()
     assert pool.error_flags() == 0
+    # the same attention kernels with fp32 outputs on the same partition streams (after the step's
+    # append, so over the same pool): R8's strict fp32 bound below, and the step's bf16 outputs
+    # must be exactly the round-to-nearest-even of these (same fp32 value, one rounding)
+    _, _, sd, sp = part.query(split)
+    o_pf32 = torch.empty((pf_spec.total_new, Hq, d), dtype=torch.float32, device="cuda")
+    o_dc32 = torch.empty((B, Hq, d), dtype=torch.float32, device="cuda")
+    mux.mux_prefill_attn(pool, 0, s_pf._keep[0], Hq, _to_dev(pside.q), o_pf32, None, scale=scale, stream=sp)
+    mux.mux_decode_attn(pool, 0, s_dc._keep[0], Hq, _to_dev(dq), o_dc32, None, scale=scale, num_splits=ns, ws=ws,
+                        stream=sd)
+    torch.cuda.synchronize()
+    assert torch.equal(o_pf32.to(torch.bfloat16), o_pf), "prefill bf16 output != rne(fp32 output)"
+    assert torch.equal(o_dc32.to(torch.bfloat16), o_dc), "decode bf16 output != rne(fp32 output)"
 
-    # ---- oracle on the samples
-    prow = synth.sample_rows(pf_spec.total_new, 24)
+    # ---- oracle on the samples (512 rows at cfg5, >= 128 at cfg2-4, late tiles included)
+    prow = synth.sample_rows_tiles(pf_spec.total_new, 512 if cfg == 5 else 160)
+    assert (prow >= pf_spec.total_new - 4 * 128).sum() >= 8
     os_ = oracle_build_side(pside, sum(pf_spec.pages_needed()) + 1, 3, Hkv, d)
     ref_p, _ = oracle.attention(pside.q, os_["kpool"], os_["vpool"], os_["qo_indptr"], os_["kv_len"],
                                 os_["page_indptr"], os_["page_ids"], scale, rows=prow)
     got_p = o_pf.float().cpu().numpy()[prow]
-    check_close(got_p, ref_p, what=f"cfg{cfg} prefill sampled rows")
+    check_close(got_p, ref_p, what=f"cfg{cfg} prefill sampled rows", out_bf16=True)
+    check_close(o_pf32.cpu().numpy()[prow], ref_p, what=f"cfg{cfg} prefill sampled rows (fp32 out)")
     sub = SideData(SideSpec([L_dc[b] - 1 for b in samp], [1] * len(samp)), dq[samp],
                    [host[b][0] for b in samp], [host[b][1] for b in samp])
     od = oracle_build_side(sub, sum(sub.spec.pages_needed()) + 1, 4, Hkv, d)
     ref_d, _ = oracle.attention(sub.q, od["kpool"], od["vpool"], od["qo_indptr"], od["kv_len"],
                                 od["page_indptr"], od["page_ids"], scale)
     got_d = o_dc.float().cpu().numpy()[samp]
-    check_close(got_d, ref_d, what=f"cfg{cfg} decode sampled sequences")
+    check_close(got_d, ref_d, what=f"cfg{cfg} decode sampled sequences", out_bf16=True)
+    check_close(o_dc32.cpu().numpy()[samp], ref_d, what=f"cfg{cfg} decode sampled sequences (fp32 out)")
     # out-projection of the same samples (R22: bf16(O) . W_o)
     for got_y, ref_o in ((y_pf.cpu().numpy()[prow], ref_p), (y_dc.cpu().numpy()[samp], ref_d)):
         ob = synth.f32_to_bf16_bits(ref_o.reshape(ref_o.shape[0], -1).astype(np.float32))

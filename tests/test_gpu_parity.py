@@ -90,6 +90,11 @@ DECODE_CASES = [
     (128, 4, 1, [3000, 17]),                           # one kv head: 8 warps share its pages (16-stage ring)
     (64, 8, 2, [2100]),                                # g = 4, two kv heads per CTA
     (128, 16, 8, [700, 1]),                            # g = 2
+    (128, 8, 4, [1000, 5, 64]),                        # Hkv = 4 (2-GPU shard of Llama-8B), g = 2: HG = 4
+    (128, 32, 4, [4096, 33]),                          # Hkv = 4 (2-GPU shard of Llama-70B), g = 8: HG = 4
+    (128, 12, 6, [600, 17]),                           # Hkv = 6: HG = 2 (largest power of two dividing 6)
+    (64, 24, 6, [300]),                                # Hkv = 6, g = 4, d64
+    (128, 9, 3, [200, 31]),                            # Hkv = 3, g = 3: HG = 1
 ]
 
 
@@ -106,7 +111,7 @@ def test_decode_parity(mux, case, splits):
 def test_decode_bf16_output_and_outliers(mux):
     side = _side(20, SideSpec([700, 63], [1, 1]), 32, 8, 128, decode=True, outliers=True)
     o, lse, ref, ref_lse, _ = _run(mux, side, 32, 8, 128, decode=True, o_f32=False)
-    check_close(o, ref, what="decode bf16 out")
+    check_close(o, ref, what="decode bf16 out", out_bf16=True)
     assert np.max(np.abs(lse - ref_lse)) <= 1e-3
 
 
@@ -119,6 +124,10 @@ PREFILL_CASES = [
     (128, 8, 1, [1000], [129]),                       # long prefix, g = 8
     (64, 4, 4, [5], [260]),                           # MHA, d64
     (128, 4, 2, [127, 129], [128, 255]),              # diagonal straddles two KV tiles
+    (128, 4, 4, [30, 0], [200, 129]),                 # MHA d128: prefill_kernel<128, 1> (one q head per CTA)
+    (128, 6, 2, [0, 50, 16], [140, 77, 1]),           # g = 3 d128: prefill_kernel<128, 1>
+    (64, 6, 2, [20], [150]),                          # g = 3 d64: prefill_kernel<64, 1>
+    (128, 12, 6, [17], [130]),                        # Hkv = 6, g = 2 (head pairs)
 ]
 
 
@@ -134,7 +143,7 @@ def test_prefill_parity(mux, case):
 def test_prefill_bf16_output_outliers(mux):
     side = _side(40, SideSpec([90], [200]), 8, 2, 128, outliers=True)
     o, lse, ref, ref_lse, _ = _run(mux, side, 8, 2, 128, decode=False, o_f32=False)
-    check_close(o, ref, what="prefill bf16 out")
+    check_close(o, ref, what="prefill bf16 out", out_bf16=True)
 
 
 # ----------------------------------------------------------------------------- invariants on GPU
@@ -157,6 +166,97 @@ def test_gpu_deterministic_run_to_run(mux):
     mux.mux_prefill_attn(gs["pool"], 0, gs["batch"], 8, gs["q"], o2, None)
     torch.cuda.synchronize()
     np.testing.assert_array_equal(o1, o2.cpu().numpy())
+
+
+def test_decode_deterministic_run_to_run(mux):
+    """R17: decode outputs are bitwise run-to-run deterministic, unsplit and split (no float
+    atomics in the split-KV merge or the combine)."""
+    import torch
+    side = _side(56, SideSpec([4000, 700, 15], [1, 1, 1]), 32, 8, 128, decode=True)
+    for ns in (1, 5):
+        o1, l1, _, _, gs = _run(mux, side, 32, 8, 128, decode=True, num_splits=ns)
+        for _ in range(3):
+            o2 = torch.empty((3, 32, 128), dtype=torch.float32, device="cuda")
+            l2 = torch.empty((3, 32), dtype=torch.float32, device="cuda")
+            ws = torch.empty(max(16, mux.mux_decode_workspace_bytes(3, 32, 128, ns)), dtype=torch.uint8, device="cuda")
+            mux.mux_decode_attn(gs["pool"], 0, gs["batch"], 32, gs["q"], o2, l2, num_splits=ns, ws=ws)
+            torch.cuda.synchronize()
+            np.testing.assert_array_equal(o1, o2.cpu().numpy())
+            np.testing.assert_array_equal(l1, l2.cpu().numpy())
+
+
+def _shared_prefix_pools(mux, Hq, Hkv, d, r, n_a, n_b, decode):
+    """Two sequences A, B with the same cached prefix of r tokens (r a multiple of 16).  Layout 1:
+    B's page table ALIASES A's r/16 prefix pages (mux_pool_share_pages, refcount 2); layout 2:
+    private copies.  Returns (outputs, oracle reference) of both layouts."""
+    import torch
+    from synth import indptr
+    g = synth.rng(57, synth.T_K_PF)
+    pre_k = synth.bf16_normal(g, (r, Hkv, d))
+    pre_v = synth.bf16_normal(g, (r, Hkv, d))
+    rows = {}
+    for name, n in (("a", n_a), ("b", n_b)):
+        rows[name] = (synth.bf16_normal(g, (n, Hkv, d)), synth.bf16_normal(g, (n, Hkv, d)),
+                      synth.bf16_normal(g, (n, Hq, d)))
+    q = np.concatenate([rows["a"][2], rows["b"][2]])
+    npre = r // 16
+    scale = 1.0 / math.sqrt(d)
+    outs = []
+    pages_total = 64
+    for shared in (True, False):
+        kst = torch.full((1, pages_total, Hkv, 16, d), 0x7FC0, dtype=torch.int16, device="cuda").view(torch.bfloat16)
+        pool = mux.Pool(1, pages_total, Hkv, d, 21, kst, kst.clone())
+        la, lb = r + n_a, r + n_b
+        pa = pool.alloc((la + 15) // 16)
+        dev = lambda a: torch.from_numpy(np.ascontiguousarray(a).view(np.int16)).cuda().view(torch.bfloat16)  # noqa: E731
+        # prefix rows: written once by A (then shared read-only with B), or into both private copies
+        mux.mux_append_kv(pool, 0, mux.Batch([0, r], [r], [0, npre], pa[:npre]), dev(pre_k), dev(pre_v))
+        if shared:
+            pool.share(pa[:npre])
+            pb = pa[:npre] + pool.alloc((lb + 15) // 16 - npre)
+            assert all(pool.refcount(x) == 2 for x in pa[:npre])
+        else:
+            pb = pool.alloc((lb + 15) // 16)
+            mux.mux_append_kv(pool, 0, mux.Batch([0, r], [r], [0, npre], pb[:npre]), dev(pre_k), dev(pre_v))
+        # new rows into each sequence's own (refcount-1) pages; a write into a shared page is rejected
+        kn = np.concatenate([rows["a"][0], rows["b"][0]])
+        vn = np.concatenate([rows["a"][1], rows["b"][1]])
+        batch = mux.Batch([0, n_a, n_a + n_b], [la, lb], [0, len(pa), len(pa) + len(pb)], pa + pb)
+        mux.mux_append_kv(pool, 0, batch, dev(kn), dev(vn))
+        T = n_a + n_b
+        o = torch.empty((T, Hq, d), dtype=torch.float32, device="cuda")
+        if decode:
+            ws = torch.empty(max(16, mux.mux_decode_workspace_bytes(2, Hq, d, 3)), dtype=torch.uint8, device="cuda")
+            mux.mux_decode_attn(pool, 0, batch, Hq, dev(q), o, None, num_splits=3, ws=ws)
+        else:
+            mux.mux_prefill_attn(pool, 0, batch, Hq, dev(q), o, None)
+        torch.cuda.synchronize()
+        outs.append(o.cpu().numpy())
+        if shared:
+            # the oracle reads the same aliased page table from the library's pool image
+            kimg = pool.k[0].view(torch.int16).cpu().numpy().view(np.uint16)
+            vimg = pool.v[0].view(torch.int16).cpu().numpy().view(np.uint16)
+            ref, _ = oracle.attention(q, kimg, vimg, np.array([0, n_a, T], np.int32), np.array([la, lb], np.int32),
+                                      np.array([0, len(pa), len(pa) + len(pb)], np.int32),
+                                      np.array(pa + pb, np.int32), scale)
+            with pytest.raises(mux.MuxError) as e:   # B's append into the aliased prefix page
+                mux.mux_append_kv(pool, 0, mux.Batch([0, 1], [r], [0, npre], pb[:npre]), dev(kn[:1]), dev(vn[:1]))
+            assert e.value.code == 4
+        pool.close()
+    return outs, ref
+
+
+@pytest.mark.parametrize("decode", [False, True])
+def test_shared_prefix_pages_gpu(mux, decode):
+    """SURVEY §8(c) invariant (i), prefix reuse across requests: two sequences
+    whose page tables alias the same full prefix pages (refcount 2) give bitwise the rows they
+    give with private copies (reduction order depends only on logical positions), and match the
+    oracle reading the aliased table."""
+    Hq, Hkv, d = 8, 2, 128
+    (o_sh, o_priv), ref = _shared_prefix_pools(mux, Hq, Hkv, d, r=160, n_a=1 if decode else 190,
+                                               n_b=1 if decode else 77, decode=decode)
+    np.testing.assert_array_equal(o_sh, o_priv)
+    check_close(o_sh, ref, what=f"shared prefix ({'decode' if decode else 'prefill'})")
 
 
 def test_prefix_reuse_equals_recompute_gpu(mux):
@@ -229,7 +329,7 @@ def test_outproj_parity(mux, T, K, N):
     mux.mux_outproj(xd, wd, yb)
     torch.cuda.synchronize()
     check_close(y.cpu().numpy(), ref, atol=1e-4, rtol=1e-4, what="outproj f32")
-    check_close(yb.float().cpu().numpy(), ref, what="outproj bf16")
+    check_close(yb.float().cpu().numpy(), ref, what="outproj bf16", out_bf16=True)
 
 
 def test_outproj_sharded_sum_equals_full(mux):
