@@ -6,21 +6,26 @@ sequences at context 4096, on disjoint green-context SM partitions (SM-split swe
 the 8 configs of the 16-SM rule).
 
 A STEP is one multiplexed window through the whole hot path (all §8(a) rows):
-  decode side : `iters` decode iterations x 32 layers, each layer = mux_append_kv (the
-                current token) + split-KV decode attention (+ combine) + out-projection
-                partial GEMM (+ NCCL all-reduce of it on the decode communicator when N > 1);
-  prefill side: the 8k prefill through all 32 layers, layer by layer, each layer =
-                mux_append_kv (8192 new K/V rows) + tcgen05 prefill attention + out-projection
+  decode side : D decode layers of the batch, each = mux_append_kv (the current token) +
+                split-KV decode attention (+ combine) + out-projection partial GEMM (+ NCCL
+                all-reduce of it, enqueued by libmux on the side's stream, when N > 1); a decode
+                iteration is N_T layers and step k continues at layer (k * D) mod N_T, so the
+                two sides balance at LAYER granularity (the N_PL idea of P:666), not in whole
+                iterations;
+  prefill side: the prefill through all N_T layers, layer by layer, each layer =
+                mux_append_kv (the new K/V rows) + tcgen05 prefill attention + out-projection
                 (+ all-reduce on the prefill communicator when N > 1),
-both enqueued by ONE mux_run_layer call (decode first) on the chosen SM split.
-`iters` balances the two sides with the paper's N_PL rule evaluated on the
-isolated timings of that split, so neither side idles (bubble-less).
+both enqueued by ONE mux_run_layer call (decode first) on the chosen SM split.  D is
+picked from the isolated per-layer times of each split (and measured around that balance point,
+since contention slows the decode side more), so neither partition idles (bubble ratio reported).
 
-metric value = model-equivalent attention tok/s = (8192 + 64*iters) tokens / step time
-(each token passes all 32 attention layers).  e2e = the same through the public API with
-the step's inputs (new-token Q/K/V, one layer's worth, reused by every layer: the QKV
-projections are outside this hot path) copied from pinned host memory and the last
-layer's outputs copied back inside the timed region.
+metric value = model-equivalent attention tok/s = (prefill tokens + B * D / N_T) / step time
+(each prefill token passes all N_T layers; D layers of a decode batch of B are B * D / N_T
+model tokens).  e2e = the same through the public API with the step's inputs (new-token Q/K/V,
+one layer's worth, reused by every layer: the QKV projections are outside this hot path) copied
+from pinned host memory and the last layer's outputs copied back inside the timed region.
+roofline / roofline_decode: the dominant kernels' launches INSIDE the timed steps, timed by CUDA
+events libmux records on the launching partition stream (mux_side.attn_events).
 
 Multi-GPU (torchrun, N>1): KV-head sharding (§8(e)) — each rank holds Hkv/N kv heads,
 Hq/N q heads and the matching rows of W_o of the same workload (strong scaling); attention
@@ -183,11 +188,14 @@ class Workload:
         self.w_o = mux.mux_outproj_pack_w(w_o)  # weight prep (once, untimed): tile-packed layout
         self.pf_y = torch.empty((Tp, self.hidden), dtype=torch.bfloat16, device=dev)
         self.dc_y = torch.empty((Bd, self.hidden), dtype=torch.bfloat16, device=dev)
-        self.hooks = {}
+        self.ar = {}
         self.scale = 1.0 / math.sqrt(self.d)
         self.ws = None
 
-    def sides(self, part_sms_dec: int, iters: int):
+    def sides(self, part_sms_dec: int, dc_layers: int, dc_layer0: int = 0, pf_events=None, dc_events=None):
+        """The step's two mux_sides: the prefill through all N_T layers, and `dc_layers` decode layers
+        starting at pool layer dc_layer0 (a decode iteration is N_T layers; a step may end inside one
+        and the next step continues it, so the two sides balance at layer granularity)."""
         mux = self.mux
         import torch
         ns = mux.mux_decode_num_splits(self.dc_spec.num_seqs, self.Hkv, max(self.dc_spec.L), part_sms_dec,
@@ -197,16 +205,17 @@ class Workload:
             self.ws = torch.empty(max(16, wsb), dtype=torch.uint8, device="cuda")
         pf = mux.make_side(self.pf_batch, self.Hq, self.pf_q, self.pf_o, k_new=self.pf_k, v_new=self.pf_v,
                            scale=self.scale, layer0=0, num_layers=self.layers, append=True,
-                           w_o=self.w_o, y=self.pf_y, hook=self.hooks.get(1))
+                           w_o=self.w_o, y=self.pf_y, allreduce=self.ar.get(1), attn_events=pf_events)
         dc = mux.make_side(self.dc_batch, self.Hq, self.dc_q, self.dc_o, k_new=self.dc_k, v_new=self.dc_v,
-                           scale=self.scale, layer0=0, num_layers=self.layers * iters, append=True,
-                           num_splits=ns, ws=self.ws, w_o=self.w_o, y=self.dc_y, hook=self.hooks.get(0))
+                           scale=self.scale, layer0=dc_layer0 % self.layers, num_layers=dc_layers, append=True,
+                           num_splits=ns, ws=self.ws, w_o=self.w_o, y=self.dc_y, allreduce=self.ar.get(0),
+                           attn_events=dc_events)
         return pf, dc, ns
 
-    def set_allreduce_hooks(self, comms):
-        """Per-layer all-reduce of this buffer set's y on each side's own stream (a7, R23)."""
-        self.hooks = {0: lambda side, layer, stream: comms[0].all_reduce_(self.dc_y, stream),
-                      1: lambda side, layer, stream: comms[1].all_reduce_(self.pf_y, stream)}
+    def set_allreduce(self, comms):
+        """Per-layer all-reduce of each side's out-projection partial sums (a7, R23), enqueued by
+        libmux from C on the side's own stream through one NCCL communicator per side."""
+        self.ar = {0: comms[0].c_allreduce(), 1: comms[1].c_allreduce()}
 
     def outproj_flops_layer(self, side):
         return 2.0 * side.total_new * self.Hq * self.d * self.hidden
@@ -289,10 +298,10 @@ def time_kernel_alone(mux, part, wl, split, which, reps=5):
     return a.elapsed_time(b) / reps * 1e-3
 
 
-def time_side(mux, part, split, wl, which, iters, reps=3):
+def time_side(mux, part, split, wl, which, dc_layers, reps=3):
     """Isolated time (s) of one side on `split` (the other side NULL)."""
     import torch
-    pf, dc, _ = wl.sides(part.query(split)[0], iters)
+    pf, dc, _ = wl.sides(part.query(split)[0], dc_layers)
     st = torch.cuda.current_stream()
     for _ in range(2):
         mux.mux_run_layer(part, split, wl.pool, pf if which == "pf" else None, dc if which == "dc" else None)
@@ -379,6 +388,94 @@ def cpu_baseline_sample(config: int):
                       f"x {S.n_layers_model} layers"}
 
 
+# ----------------------------------------------------------------------------- measurement helpers
+def time_tc_share(mux, part, wl, split, pf_sms, reps=5):
+    """TC(k_p): a dense bf16 GEMM (libmux's tcgen05 out-projection GEMM, T=8192 x
+    K=Hq*d x N=hidden, sized for the partition's SMs) timed with CUDA events on the prefill
+    partition's own stream, nothing else running.  Returns TFLOP/s."""
+    import torch
+    raw = part.query(split)[3] if split >= 0 else torch.cuda.current_stream().cuda_stream
+    st = torch.cuda.ExternalStream(raw)
+    T = 8192
+    x = torch.randn((T, wl.Hq * wl.d), device="cuda").to(torch.bfloat16)
+    y = torch.empty((T, wl.hidden), dtype=torch.bfloat16, device="cuda")
+    torch.cuda.synchronize()
+    for _ in range(2):
+        mux.mux_outproj(x, wl.w_o, y, stream=raw, num_sms=pf_sms)
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    a.record(st)
+    for _ in range(reps):
+        mux.mux_outproj(x, wl.w_o, y, stream=raw, num_sms=pf_sms)
+    b.record(st)
+    torch.cuda.synchronize()
+    t = a.elapsed_time(b) / reps * 1e-3
+    return 2.0 * T * wl.Hq * wl.d * wl.hidden / t / 1e12
+
+
+def host_cpu_model():
+    try:
+        out = subprocess.run(["lscpu"], capture_output=True, text=True, timeout=10).stdout
+        for line in out.splitlines():
+            if line.lower().startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except Exception:
+        pass
+    return None
+
+
+def oracle_1thread():
+    """The oracle on ONE thread (OMP_NUM_THREADS=1, run in a subprocess): the whole cfg1 step (one
+    layer) and the whole cfg2 decode side of one layer (64 x 4096), as model tok/s."""
+    import oracle
+    import synth
+    from synth import indptr
+    from oracle.alloc import OraclePagePool, build_page_tables
+    out = {"threads": oracle.num_threads()}
+
+    def side_time(cfg, spec, decode):
+        c = synth.get_config(cfg)
+        S = c.shapes
+        sd = synth.make_side(cfg, S, spec, decode=decode)
+        pool = OraclePagePool(sum(spec.pages_needed()) + 1, 1)
+        ind, ids = build_page_tables(pool, spec.pages_needed())
+        k, v = oracle.empty_pool(len(ids) + 1, S.Hkv, S.d, poison=False)
+        oracle.append(k, v, np.concatenate(sd.k_rows), np.concatenate(sd.v_rows), indptr(spec.L),
+                      np.array(spec.L, np.int32), np.array(ind, np.int32), np.array(ids, np.int32))
+        t0 = time.perf_counter()
+        oracle.attention(sd.q, k, v, indptr(spec.n), np.array(spec.L, np.int32), np.array(ind, np.int32),
+                         np.array(ids, np.int32), 1 / math.sqrt(S.d))
+        return time.perf_counter() - t0
+
+    c1 = synth.get_config(1)
+    t1 = side_time(1, c1.prefill, False) + side_time(1, c1.decode, True)
+    out["cfg1_step_s"] = t1
+    out["cfg1_tok_s"] = (c1.prefill.total_new + c1.decode.num_seqs) / t1
+    c2 = synth.get_config(2)
+    t2 = side_time(2, c2.decode, True)
+    out["cfg2_decode_layer_s"] = t2
+    out["cfg2_decode_tok_s"] = c2.decode.num_seqs / (t2 * c2.shapes.n_layers_model)
+    return out
+
+
+def bubble_stats(tt):
+    """R21: idle share of each side's partition over the timed steps, from the
+    %globaltimer stamps [steps][dec_start, dec_end, pf_start, pf_end]: per step (1 - side busy /
+    step window) and over the whole region (1 - sum of side busy / first start .. last end)."""
+    tt = np.asarray(tt, dtype=np.float64)
+    w0 = np.minimum(tt[:, 0], tt[:, 2])
+    w1 = np.maximum(tt[:, 1], tt[:, 3])
+    dec, pf = tt[:, 1] - tt[:, 0], tt[:, 3] - tt[:, 2]
+    step_dec = float(np.mean(1 - dec / (w1 - w0)))
+    step_pf = float(np.mean(1 - pf / (w1 - w0)))
+    span = w1.max() - w0.min()
+    reg_dec = float(1 - dec.sum() / span)
+    reg_pf = float(1 - pf.sum() / span)
+    return {"bubble_ratio": (reg_dec + reg_pf) / 2, "bubble_ratio_dec": reg_dec, "bubble_ratio_pf": reg_pf,
+            "per_step_dec": step_dec, "per_step_pf": step_pf,
+            "def": "idle share of each side's partition between the first and last stamp of the timed "
+                   "steps (P:1019-1022), averaged over the two sides; per_step_* = within each step's window"}
+
+
 # ----------------------------------------------------------------------------- main arm
 def main():
     ap = argparse.ArgumentParser()
@@ -386,17 +483,24 @@ def main():
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="mux", choices=["mux", "reference"])
-    ap.add_argument("--config", type=int, default=2)
+    ap.add_argument("--config", type=int, default=0, help="BASELINE config (default: 2 at N=1, 4 at N>1)")
     ap.add_argument("--layers", type=int, default=0, help="pool layers (default: the model's N_T)")
     ap.add_argument("--split", type=int, default=-2, help="split index; -2 = sweep and pick the best")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--granularity", type=int, default=8, help="decode SM step of the split sweep")
+    ap.add_argument("--oracle-1thread", action="store_true", help=argparse.SUPPRESS)
     args = ap.parse_args()
     args.warmup = max(3, args.warmup)
+    if args.oracle_1thread:
+        print(json.dumps(oracle_1thread()))
+        return
 
     rank = int(os.environ.get("RANK", 0))
     world = int(os.environ.get("WORLD_SIZE", 1))
     local = int(os.environ.get("LOCAL_RANK", 0))
+    if not args.config:
+        # N=1: BASELINE's single-B200 SM-split sweep config; N>1: its KV-head-sharded 70B config
+        args.config = 2 if world == 1 else 4
     if args.impl == "reference":
         run_reference(args, rank, world)
         return
@@ -405,21 +509,22 @@ def main():
     import torch.distributed as dist
     torch.cuda.set_device(local)
     if world > 1:
+        os.environ.setdefault("NCCL_DEBUG", "INFO")   # communicator init lines (nranks) stay visible
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     import paper_2504_14489_b200 as mux
     mux.lib()
     peaks, peaks_src = load_peaks()
 
     wl = Workload(args.config, rank, world, layers=args.layers or None)
+    NT = wl.layers
     comms = []
     if world > 1:
-        # one NCCL communicator per side; each layer's out-proj partial sums are all-reduced on
-        # the side's own (green-context) stream from the mux_run_layer hook
+        # one NCCL communicator per side; libmux enqueues each layer's all-reduce of the out-proj
+        # partial sums from C on the side's own (green-context) stream (mux_side.ar_fn / ar_comm)
         from paper_2504_14489_b200 import nccl
         comms = [nccl.Comm(rank, world), nccl.Comm(rank, world)]
-        wl.set_allreduce_hooks(comms)
-    if world > 1:  # identical page tables on every rank (integer-exact check)
-        h = torch.tensor([wl.page_hash], device="cuda")
+        wl.set_allreduce(comms)
+        h = torch.tensor([wl.page_hash], device="cuda")   # identical page tables on every rank
         hs = [torch.zeros_like(h) for _ in range(world)]
         dist.all_gather(hs, h)
         assert all(int(x) == wl.page_hash for x in hs), "page tables differ across ranks"
@@ -429,26 +534,32 @@ def main():
     # its cluster kernels; these kernels use no clusters, and green contexts split in 8s)
     configs = mux.mux_partition_configs(total_sms, args.granularity, 12)
     part = mux.Partition(local, configs)
-    # ---- calibration (untimed): isolated side times per split, N_PL balance, predicted mux rate
+    Bd = wl.dc_spec.num_seqs
+
+    def step_tokens(dc_layers):
+        # model-equivalent tokens: every prefill token passes all N_T layers; a decode token needs
+        # N_T layers, so dc_layers decode layers of a batch of Bd are Bd * dc_layers / N_T tokens
+        return wl.pf_spec.total_new + Bd * dc_layers / NT
+
+    # ---- calibration (untimed): isolated side times per split, layer-granular balance (N_PL idea,
+    # decode layers per whole prefill so both partitions stay busy), measured mux rate
     sweep = []
-    full_pf = time_side(mux, part, -1, wl, "pf", 1)
-    full_dc = time_side(mux, part, -1, wl, "dc", 1)
+    full_pf = time_side(mux, part, -1, wl, "pf", NT)
+    full_dc = time_side(mux, part, -1, wl, "dc", NT)
     splits = range(len(configs)) if args.split == -2 else [args.split]
     for i in splits:
         dsms, psms, _, _ = part.query(i)
-        t_dc = time_side(mux, part, i, wl, "dc", 1)          # one decode iteration (N_T layers)
-        t_pf = time_side(mux, part, i, wl, "pf", 1)          # the whole prefill (N_T layers)
-        # decode iterations per whole prefill = N_T / N_PL from the isolated times; both
-        # neighbours of the ratio, and one fewer (contention slows the decode side more than the
-        # prefill side in the mux window), are measured below and the fastest kept
-        r = t_pf / t_dc
-        for iters in sorted({max(1, math.floor(r) - 1), max(1, math.floor(r)), max(1, math.ceil(r))}):
+        t_dc = time_side(mux, part, i, wl, "dc", NT)          # one decode iteration (N_T layers)
+        t_pf = time_side(mux, part, i, wl, "pf", NT)          # the whole prefill (N_T layers)
+        r = t_pf / (t_dc / NT)                                 # decode layers per prefill window
+        # contention slows the decode side more than the prefill side: candidates below r too
+        for f in (0.8, 0.9, 1.0):
             sweep.append({"split": i, "dec_sms": dsms, "pf_sms": psms, "t_dc_iso_ms": t_dc * 1e3,
-                          "t_pf_iso_ms": t_pf * 1e3, "iters": iters})
+                          "t_pf_iso_ms": t_pf * 1e3, "dc_layers": max(1, int(round(r * f)))})
 
     def measure_mux(entry, reps=3):
-        i, iters = entry["split"], entry["iters"]
-        pf, dc, ns = wl.sides(entry["dec_sms"], iters)
+        i, D = entry["split"], entry["dc_layers"]
+        pf, dc, ns = wl.sides(entry["dec_sms"], D)
         times = torch.zeros(4, dtype=torch.int64, device="cuda")
         for _ in range(2):
             mux.mux_run_layer(part, i, wl.pool, pf, dc, times)
@@ -462,54 +573,80 @@ def main():
         torch.cuda.synchronize()
         t = a.elapsed_time(b) / reps * 1e-3
         tt = times.cpu().numpy()
-        toks = wl.pf_spec.total_new + wl.dc_spec.num_seqs * iters
-        entry.update({"t_mux_ms": t * 1e3, "tok_s": toks / t,
+        entry.update({"t_mux_ms": t * 1e3, "tok_s": step_tokens(D) / t,
                       "dec_side_ms": (tt[1] - tt[0]) * 1e-6, "pf_side_ms": (tt[3] - tt[2]) * 1e-6,
-                      "slowdown_dec": (tt[1] - tt[0]) * 1e-9 / (entry["t_dc_iso_ms"] * 1e-3 * iters),
+                      "slowdown_dec": (tt[1] - tt[0]) * 1e-9 / (entry["t_dc_iso_ms"] * 1e-3 * D / NT),
                       "slowdown_pf": (tt[3] - tt[2]) * 1e-9 / (entry["t_pf_iso_ms"] * 1e-3),
                       "num_splits": ns})
         return entry
 
-    for e in sweep:
+    seen = set()
+    for e in list(sweep):
+        key = (e["split"], e["dc_layers"])
+        if key in seen:
+            sweep.remove(e)
+            continue
+        seen.add(key)
         measure_mux(e)
     best = max(sweep, key=lambda e: e["tok_s"])
     if world > 1:  # every rank must run the same split: rank 0 decides
         t = torch.tensor([sweep.index(best)], device="cuda")
         dist.broadcast(t, 0)
         best = sweep[int(t.item())]
-    i, iters = best["split"], best["iters"]
-    pf, dc, ns = wl.sides(best["dec_sms"], iters)
-    times = torch.zeros(4, dtype=torch.int64, device="cuda")
+    i, D = best["split"], best["dc_layers"]
     st = torch.cuda.current_stream()
+    K = args.steps
 
-    # ---- timed region: K steps (inputs resident in HBM; pool per layer >> L2)
-    for _ in range(args.warmup):
-        mux.mux_run_layer(part, i, wl.pool, pf, dc, times)
+    # ---- timed region: K steps (inputs resident in HBM; the pool per layer is >> L2 except cfg1,
+    # which flushes L2 between steps).  Step k's decode side continues at layer (k * D) mod N_T.
+    # CUDA events around every attention launch, recorded by libmux on the side's own stream.
+    ev_pf = [mux.EventSet(2 * NT) for _ in range(K)]
+    ev_dc = [mux.EventSet(2 * D) for _ in range(K)]
+    step_sides = [wl.sides(best["dec_sms"], D, (k * D) % NT, ev_pf[k], ev_dc[k]) for k in range(K)]
+    ns = step_sides[0][2]
+    warm_sides = [wl.sides(best["dec_sms"], D, (k * D) % NT) for k in range(args.warmup)]
+    times = torch.zeros((K, 4), dtype=torch.int64, device="cuda")
+    wtimes = torch.zeros(4, dtype=torch.int64, device="cuda")
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda") if args.config == 1 else None
+    for k in range(args.warmup):
+        mux.mux_run_layer(part, i, wl.pool, warm_sides[k][0], warm_sides[k][1], wtimes)
     torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
     a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    side_ms = []
+    sa = [torch.cuda.Event(enable_timing=True) for _ in range(K)]
+    sb = [torch.cuda.Event(enable_timing=True) for _ in range(K)]
     with ClockSampler(local) as clk:
         torch.cuda.synchronize()
         a.record(st)
-        step_ev = []
-        for _ in range(args.steps):
-            mux.mux_run_layer(part, i, wl.pool, pf, dc, times)
-            step_ev.append(torch.cuda.Event(enable_timing=True))
-            step_ev[-1].record(st)
+        for k in range(K):
+            if flush is not None:
+                flush.zero_()                       # evict L2 (126 MB) before the step (cfg1 only)
+            sa[k].record(st)
+            mux.mux_run_layer(part, i, wl.pool, step_sides[k][0], step_sides[k][1], times[k])
+            sb[k].record(st)
         b.record(st)
         torch.cuda.synchronize()
     tt = times.cpu().numpy()
-    t_step = a.elapsed_time(b) / args.steps * 1e-3
-    step_ms = [a.elapsed_time(step_ev[0])] + [step_ev[k - 1].elapsed_time(step_ev[k]) for k in range(1, len(step_ev))]
+    step_ms = [sa[k].elapsed_time(sb[k]) for k in range(K)]
+    t_step = float(np.mean(step_ms)) * 1e-3 if flush is not None else a.elapsed_time(b) / K * 1e-3
+    pf_attn_ms = np.concatenate([e.durations_ms(NT) for e in ev_pf])
+    dc_attn_ms = np.concatenate([e.durations_ms(D) for e in ev_dc])
+    bub = bubble_stats(tt)
+    hot = None
+    if flush is not None:   # cfg1 also hot (back to back, no flush)
+        a.record(st)
+        for k in range(K):
+            mux.mux_run_layer(part, i, wl.pool, step_sides[k][0], step_sides[k][1], times[k])
+        b.record(st)
+        torch.cuda.synchronize()
+        hot = step_tokens(D) / (a.elapsed_time(b) / K * 1e-3)
     if world > 1:
         tm = torch.tensor([t_step], device="cuda", dtype=torch.float64)
         dist.all_reduce(tm, op=dist.ReduceOp.MAX)
         t_step = float(tm.item())
         dist.barrier()
-    toks = wl.pf_spec.total_new + wl.dc_spec.num_seqs * iters
-    value = toks / t_step  # tokens are whole-model tokens (all N_T layers); aggregate over ranks (head shards)
+    value = step_tokens(D) / t_step   # aggregate over ranks (each rank holds a head shard of the same tokens)
 
     # ---- e2e through the public API: every step copies its inputs (new-token Q/K/V) from pinned
     # host memory and its outputs (y of both sides) back.  Double-buffered like a server: step
@@ -521,10 +658,15 @@ def main():
     for k in names_in + ("pf_o", "dc_o", "pf_y", "dc_y"):
         setattr(wl2, k, torch.empty_like(getattr(wl, k)))
     wl2.ws = None
-    if comms:
-        wl2.set_allreduce_hooks(comms)
     sets = [wl, wl2]
-    sides2 = [(pf, dc), wl2.sides(best["dec_sms"], iters)[:2]]
+    e2e_sides = {}
+
+    def e2e_side(c, step):
+        key = (c, (step * D) % NT)
+        if key not in e2e_sides:
+            e2e_sides[key] = sets[c].sides(best["dec_sms"], D, key[1])[:2]
+        return e2e_sides[key]
+
     outs = [[torch.empty(w.pf_y.shape, dtype=w.pf_y.dtype).pin_memory(),
              torch.empty(w.dc_y.shape, dtype=w.dc_y.dtype).pin_memory()] for w in sets]
     h2d = sum(t.numel() * t.element_size() for t in pin.values())
@@ -549,7 +691,8 @@ def main():
             if step + 1 < steps:
                 h2d_into(1 - c)                              # prefetch the next step's inputs
             st.wait_event(ev_in[c])
-            mux.mux_run_layer(part, i, wl.pool, sides2[c][0], sides2[c][1], times)
+            pfs, dcs = e2e_side(c, step)
+            mux.mux_run_layer(part, i, wl.pool, pfs, dcs, wtimes)
             ev_done[c].record(st)
             with torch.cuda.stream(cs):
                 cs.wait_event(ev_done[c])
@@ -564,98 +707,110 @@ def main():
     torch.cuda.synchronize()
     a2, b2 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     a2.record(st)
-    e2e_run(args.steps)
+    e2e_run(K)
     b2.record(st)
     torch.cuda.synchronize()
-    t_e2e = a2.elapsed_time(b2) / args.steps * 1e-3
+    t_e2e = a2.elapsed_time(b2) / K * 1e-3
     if world > 1:
         tm = torch.tensor([t_e2e], device="cuda", dtype=torch.float64)
         dist.all_reduce(tm, op=dist.ReduceOp.MAX)
         t_e2e = float(tm.item())
 
-    # ---- rooflines (achieved = algorithmic work per launch / average launch duration)
-    pf_side_s = (tt[3] - tt[2]) * 1e-9
-    dc_side_s = (tt[1] - tt[0]) * 1e-9
-    # a side's per-layer window holds append + attention + out-proj (+ all-reduce): the prefill
-    # roofline counts both tcgen05 kernels' FLOPs over the whole window (a lower bound for each)
-    pf_launch_s = pf_side_s / wl.layers
-    dc_launch_s = dc_side_s / (wl.layers * iters)
-    pf_tflops = (wl.prefill_flops_layer() + wl.outproj_flops_layer(wl.pf_spec)) / pf_launch_s / 1e12
-    dc_gbs = wl.decode_bytes_layer() / dc_launch_s / 1e9
-    tc_peak = peaks.get("bf16_tflops_sustained", peaks["bf16_tflops"])
-    traffic = {}
-    try:
-        with open(os.path.join(ROOT, "profiles", "r01s3_traffic.json")) as f:
-            traffic = json.load(f)
-    except Exception:
-        pass
+    # ---- rooflines of the dominant kernels, measured in the timed region (CUDA events on the
+    # launching partition stream; achieved = algorithmic work per launch / mean launch duration)
     pf_share = best["pf_sms"] / total_sms
     dc_share = best["dec_sms"] / total_sms
-    # SURVEY §8(d) denominator (3): BW_read(k_d), a read-only 32 KiB bulk-copy stream (mux_stream_read)
-    # on the SAME decode partition, measured here (untimed region), alone and next to the prefill side
+    pf_launch_s = float(np.mean(pf_attn_ms)) * 1e-3
+    dc_launch_s = float(np.mean(dc_attn_ms)) * 1e-3
+    pf_tflops = wl.prefill_flops_layer() / pf_launch_s / 1e12
+    dc_gbs = wl.decode_bytes_layer() / dc_launch_s / 1e9
+    burst, sustained = peaks["bf16_tflops"], peaks.get("bf16_tflops_sustained", peaks["bf16_tflops"])
+    traffic = {}
+    for tf in ("r02_traffic.json", "r01s3_traffic.json"):
+        try:
+            with open(os.path.join(ROOT, "profiles", tf)) as f:
+                traffic = json.load(f)
+            traffic["_file"] = tf
+            break
+        except Exception:
+            pass
+    # SURVEY §8(d) decode denominators: BW_read(k_d) = read-only 32 KiB bulk-copy stream on the SAME
+    # decode partition, alone and while the step's prefill side runs (contended: the primary one)
     bw_part, bw_full = probe_read_bw(mux, part, wl, i, best["dec_sms"]), probe_read_bw(mux, part, wl, -1, total_sms)
-    bw_part_mux = probe_read_bw_contended(mux, part, wl, i, best["dec_sms"], pf)
-    # the dominant kernels alone on their own partitions (CUDA events on the partition stream)
+    bw_part_mux = probe_read_bw_contended(mux, part, wl, i, best["dec_sms"], step_sides[0][0])
+    tc_kp = time_tc_share(mux, part, wl, i, best["pf_sms"])
     t_pf_k = time_kernel_alone(mux, part, wl, i, "pf")
     t_dc_k = time_kernel_alone(mux, part, wl, i, "dc")
-    roofline = {"bound": "tensor", "kernel": "prefill side per layer: prefill6_kernel + outproj2_kernel (tcgen05)",
-                "achieved": pf_tflops,
-                "peak": tc_peak, "unit": "TFLOP/s", "frac": pf_tflops / tc_peak,
-                "frac_of_sm_share": pf_tflops / (tc_peak * pf_share), "peak_src": f"{peaks_src} bf16_tflops_sustained",
-                "traffic": (traffic.get("prefill6_kernel") or traffic.get("prefill_kernel") or {}).get("bytes"),
-                "traffic_kernel": "prefill6_kernel" if "prefill6_kernel" in traffic else "prefill_kernel",
-                "kernel_alone": {"kernel": "prefill6_kernel", "sms": best["pf_sms"], "launch_us": t_pf_k * 1e6,
-                                 "achieved": wl.prefill_flops_layer() / t_pf_k / 1e12,
-                                 "peak_burst_share": peaks["bf16_tflops"] * pf_share,
-                                 "frac_of_burst_share": wl.prefill_flops_layer() / t_pf_k / 1e12
-                                 / (peaks["bf16_tflops"] * pf_share),
-                                 "frac_of_sustained_share": wl.prefill_flops_layer() / t_pf_k / 1e12 / (tc_peak * pf_share),
-                                 "note": "5 launches of layer 0 on the prefill partition stream, nothing else running, "
-                                         "right after the timed steps (same power-capped clocks); peaks scaled by the "
-                                         "partition's SM share"},
-                "per_launch": (f"1 layer: causal prefill attention {wl.prefill_flops_layer():.3e} FLOP + o_proj "
-                               f"{wl.pf_spec.total_new}x{wl.Hq * wl.d}x{wl.hidden} {wl.outproj_flops_layer(wl.pf_spec):.3e}")}
-    roofline_dec = {"bound": "hbm", "kernel": "decode_kernel", "achieved": dc_gbs, "peak": peaks["hbm_gbs"],
-                    "unit": "GB/s", "frac": dc_gbs / peaks["hbm_gbs"], "peak_src": f"{peaks_src} hbm_gbs",
-                    "sm_share": dc_share, "partition_read_gbs": bw_part, "full_gpu_read_gbs": bw_full,
-                    "frac_of_partition_read": dc_gbs / bw_part,
-                    # the same decode layer on the same partition with the prefill side idle (sweep)
-                    "iso_achieved": wl.decode_bytes_layer() / (best["t_dc_iso_ms"] * 1e-3 / wl.layers) / 1e9,
-                    "iso_frac_of_partition_read": wl.decode_bytes_layer() / (best["t_dc_iso_ms"] * 1e-3 / wl.layers)
-                    / 1e9 / bw_part,
-                    "partition_read_src": f"mux_stream_read on the {best['dec_sms']}-SM decode partition (alone)",
-                    "partition_read_gbs_contended": bw_part_mux,
-                    "frac_of_partition_read_contended": dc_gbs / bw_part_mux,
-                    "partition_read_contended_src": "the same probe while the step's prefill side runs on the "
-                                                    "prefill partition (same run, same clocks regime)",
-                    "kernel_alone": {"kernel": "decode_kernel (+ combine)", "sms": best["dec_sms"],
-                                     "launch_us": t_dc_k * 1e6, "achieved": wl.decode_bytes_layer() / t_dc_k / 1e9,
-                                     "frac_of_partition_read": wl.decode_bytes_layer() / t_dc_k / 1e9 / bw_part},
-                    "traffic": traffic.get("decode_kernel", {}).get("bytes")}
-    launches_per_step = wl.layers * 3 + wl.layers * iters * (3 + (1 if ns > 1 else 0)) + 4
-    clocks = clk.summary()
+    peak_pf = burst * pf_share
+    roofline = {"bound": "tensor", "kernel": "prefill6_kernel (tcgen05 causal prefill attention, 1 launch per layer)",
+                "achieved": pf_tflops, "peak": peak_pf, "unit": "TFLOP/s", "frac": pf_tflops / peak_pf,
+                "traffic": (traffic.get("prefill6_kernel") or {}).get("bytes"),
+                "traffic_src": traffic.get("_file"),
+                "launches": int(len(pf_attn_ms)), "launch_us_mean": pf_launch_s * 1e6,
+                "launch_us_p10_p90": [float(np.percentile(pf_attn_ms, q)) * 1e3 for q in (10, 90)],
+                "per_launch_flop": wl.prefill_flops_layer(),
+                "peak_src": f"{peaks_src} bf16_tflops (burst) {burst} x prefill SM share {best['pf_sms']}/{total_sms}",
+                "frac_of_sustained_share": pf_tflops / (sustained * pf_share),
+                "tc_kp_tflops": tc_kp, "frac_of_tc_kp": pf_tflops / tc_kp,
+                "tc_kp_src": f"libmux tcgen05 GEMM 8192x{wl.Hq * wl.d}x{wl.hidden} on the {best['pf_sms']}-SM prefill "
+                             "green context, CUDA events, alone",
+                "vendor_peak_share": 2250.0 * pf_share, "frac_of_vendor_share": pf_tflops / (2250.0 * pf_share),
+                "alone_launch_us": t_pf_k * 1e6, "alone_frac": wl.prefill_flops_layer() / t_pf_k / 1e12 / peak_pf,
+                "window": f"mean over the {len(pf_attn_ms)} prefill attention launches of the {K} timed steps "
+                          "(decode side running beside it)"}
+    roofline_dec = {"bound": "hbm", "kernel": "decode_kernel (+ combine_kernel when split)", "achieved": dc_gbs,
+                    "peak": bw_part_mux, "unit": "GB/s", "frac": dc_gbs / bw_part_mux,
+                    "peak_src": f"BW_read({best['dec_sms']}) measured on the decode partition while the prefill side runs",
+                    "traffic": (traffic.get("decode_kernel") or {}).get("bytes"), "traffic_src": traffic.get("_file"),
+                    "launches": int(len(dc_attn_ms)), "launch_us_mean": dc_launch_s * 1e6,
+                    "per_launch_bytes": wl.decode_bytes_layer(),
+                    "partition_read_alone_gbs": bw_part, "frac_of_partition_read_alone": dc_gbs / bw_part,
+                    "full_gpu_read_gbs": bw_full, "hbm_copy_gbs": peaks["hbm_gbs"],
+                    "frac_of_hbm_copy_share": dc_gbs / (peaks["hbm_gbs"] * dc_share),
+                    "vendor_hbm_gbs": 8000.0, "frac_of_vendor_hbm": dc_gbs / 8000.0,
+                    "sm_share": dc_share,
+                    "iso_achieved": wl.decode_bytes_layer() / (best["t_dc_iso_ms"] * 1e-3 / NT) / 1e9,
+                    "alone_launch_us": t_dc_k * 1e6, "alone_frac_of_partition_read": wl.decode_bytes_layer() / t_dc_k
+                    / 1e9 / bw_part}
+    per_dc_layer = 3 + (1 if ns > 1 else 0)   # append, decode, (combine), out-proj
+    launches_per_step = NT * 3 + D * per_dc_layer + 4
     line = {
-        "metric": METRIC, "value": value, "unit": "tok/s", "n_gpus": world, "steps": args.steps,
+        "metric": METRIC, "value": value, "unit": "tok/s", "n_gpus": world, "steps": K,
         "warmup": args.warmup, "ms_per_step": t_step * 1e3, "higher_is_better": True,
         "scaling": "strong" if world > 1 else "weak", "vs_baseline": None, "dtype": "bf16",
-        "data": "synthetic (seeded N(0,1) bf16 KV pool, Q/K/V; random-init shapes of Llama-3-8B attention)",
-        "config": {"workload": wl.cfg.name, "layers": wl.layers, "Hq_per_rank": wl.Hq, "Hkv_per_rank": wl.Hkv,
-                   "split": {"dec_sms": best["dec_sms"], "pf_sms": best["pf_sms"]}, "decode_iters_per_step": iters,
+        "data": "synthetic (seeded N(0,1) bf16 KV pool, Q/K/V; random-init W_o; attention shapes of "
+                + ("Llama-3-70B" if args.config == 4 else "Llama-3-8B") + ")",
+        "config": {"workload": wl.cfg.name, "layers": NT, "Hq_per_rank": wl.Hq, "Hkv_per_rank": wl.Hkv,
+                   "split": {"dec_sms": best["dec_sms"], "pf_sms": best["pf_sms"]},
+                   "decode_layers_per_step": D, "decode_iters_per_step": D / NT,
                    "decode_num_splits": ns, "parallelism": f"kv-head shard x{world}" if world > 1 else "single GPU",
-                   "l2": "inputs larger than L2 (1.1 GB of KV per layer, 32 layers rotate)"},
+                   "l2": ("L2 flushed (256 MB write) before every timed step" if flush is not None else
+                          "inputs larger than L2 (KV pool of every layer >> 126 MB; layers rotate)")},
         "roofline": roofline, "roofline_decode": roofline_dec,
-        "e2e": {"value": toks / t_e2e, "unit": "tok/s", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h},
-        "gpu_launches": launches_per_step * args.steps,
+        "bubble": bub, "bubble_ratio": bub["bubble_ratio"],
+        "e2e": {"value": step_tokens(D) / t_e2e, "unit": "tok/s", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h},
+        "gpu_launches": launches_per_step * K,
         "step_ms_p10_p50_p90": [float(np.percentile(step_ms, q)) for q in (10, 50, 90)],
-        "clocks": clocks,
-        "iso_full_gpu_ms": {"prefill_32_layers": full_pf * 1e3, "decode_iter_32_layers": full_dc * 1e3},
-        "time_sliced_tok_s": (wl.pf_spec.total_new + wl.dc_spec.num_seqs * iters) / (full_pf + iters * full_dc),
+        "clocks": clk.summary(),
+        "iso_full_gpu_ms": {"prefill_all_layers": full_pf * 1e3, "decode_iter_all_layers": full_dc * 1e3},
+        "time_sliced_tok_s": step_tokens(D) / (full_pf + full_dc * D / NT),
         "sweep": sweep,
         "partition_mem_bytes": part.memory_bytes(),
     }
+    if hot is not None:
+        line["value_hot"] = hot
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         try:
-            line["cpu_baseline"] = cpu_baseline_sample(args.config)
+            cb = cpu_baseline_sample(args.config)
+            cb["host_cpu"] = host_cpu_model()
+            try:
+                env = dict(os.environ, OMP_NUM_THREADS="1")
+                out = subprocess.run([sys.executable, os.path.abspath(__file__), "--oracle-1thread"], env=env,
+                                     capture_output=True, text=True, timeout=600).stdout.strip().splitlines()
+                cb["oracle_1thread"] = json.loads(out[-1])
+            except Exception as e:
+                cb["oracle_1thread"] = {"error": str(e)}
+            line["cpu_baseline"] = cb
         except Exception as e:  # reported, never silently replaced
             line["cpu_baseline"] = {"value": None, "error": str(e)}
     if rank == 0:

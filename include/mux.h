@@ -230,6 +230,18 @@ typedef struct {
   int32_t y_dtype;
   mux_layer_hook hook;     /* optional */
   void* hook_user;
+  /* Multi-GPU: after each layer's out-projection, y is all-reduced
+   * in place (sum, bf16, count total_q * hidden) on the side's own stream by calling ar_fn, the
+   * ncclAllReduce entry point of the NCCL library that created ar_comm (the caller dlsym's it:
+   * ncclResult_t (*)(const void*, void*, size_t, ncclDataType_t, ncclRedOp_t, ncclComm_t,
+   * cudaStream_t)).  Enqueued from C inside the layer loop (no host callback); a non-zero NCCL
+   * result returns MUX_ERR_CUDA.  NULL = no collective (single GPU).  Needs w_o. */
+  void* ar_fn;
+  void* ar_comm;
+  /* optional timing of the dominant kernels: 2 * num_layers cudaEvent_t handles (created by the
+   * caller with timing enabled), recorded on the side's stream right before and right after each
+   * layer's attention launch(es) (decode: attention + split combine).  NULL = none. */
+  void* const* attn_events;
 } mux_side;
 
 /* device timestamps (%globaltimer, ns) written by 1-thread stamp kernels on each side */
@@ -258,6 +270,10 @@ int mux_run_layer(mux_part_t part, int32_t split_idx, mux_pool_t pool,
  * (no atomics).  Errors: MUX_ERR_INVALID_ARG / MUX_ERR_UNSUPPORTED / MUX_ERR_CUDA. */
 int mux_outproj(const void* x, const void* w_packed, void* y, int32_t y_dtype, int32_t T, int32_t K,
                 int32_t N, mux_stream_t stream);
+/* the same GEMM sized for num_sms SMs (the partition `stream` runs on; <= 0 = the whole
+ * device): also the TC(k_p) dense-GEMM denominator of SURVEY §8(d) on a green context */
+int mux_outproj_sms(const void* x, const void* w_packed, void* y, int32_t y_dtype, int32_t T, int32_t K,
+                    int32_t N, mux_stream_t stream, int32_t num_sms);
 
 /* bytes of the packed layout of a [K][N] weight: ceil(N/128) * ceil(K/64) * 16384 */
 size_t mux_outproj_packed_bytes(int32_t K, int32_t N);
@@ -325,6 +341,12 @@ typedef struct {
   void* y_log;
   int32_t log_rows;
   int32_t o_f32;                /* 1: attention outputs in f32 (needs w_o == NULL); 0: bf16 */
+  /* f2 run-ahead: 1 = the next decode iteration is enqueued while the current one runs (two in
+   * flight; its batch = the current one's minus requests whose last token is already enqueued,
+   * plus merged prefills), so the decode SMs see no host turn-around gap between iterations.
+   * Valid when the next iteration's inputs are produced on the device (on-device sampling; here
+   * synthetic rows).  0 = launch after completion (the token returns to the host first). */
+  int32_t overlap;
 } mux_engine_desc;
 
 typedef struct {

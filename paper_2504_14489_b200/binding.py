@@ -51,7 +51,7 @@ class SideC(ctypes.Structure):
                 ("layer0", c_i32), ("num_layers", c_i32), ("append", c_i32), ("num_splits", c_i32),
                 ("ws", c_p), ("ws_bytes", c_sz), ("w_o", c_p), ("y", c_p), ("w_stride", c_i64),
                 ("y_stride", c_i64), ("hidden", c_i32), ("y_dtype", c_i32), ("hook", LayerHook),
-                ("hook_user", c_p)]
+                ("hook_user", c_p), ("ar_fn", c_p), ("ar_comm", c_p), ("attn_events", c_p)]
 
 
 class EngineDesc(ctypes.Structure):
@@ -59,11 +59,13 @@ class EngineDesc(ctypes.Structure):
                 ("src_rows", c_i32), ("w_o", c_p), ("hidden", c_i32), ("max_decode_seqs", c_i32),
                 ("max_prefill_tokens", c_i32), ("fixed_split", c_i32), ("n_cost", c_i32), ("dec_theta", c_p),
                 ("pf_theta", c_p), ("dec_slowdown", c_p), ("tbt_slo_us", c_dbl), ("fixed_pl", c_i32),
-                ("handoff", c_i32), ("keep_pages", c_i32), ("serialize", c_i32)]
+                ("handoff", c_i32), ("keep_pages", c_i32), ("serialize", c_i32), ("use_graphs", c_i32),
+                ("o_log", c_p), ("y_log", c_p), ("log_rows", c_i32), ("o_f32", c_i32), ("overlap", c_i32)]
 
 
 class RequestC(ctypes.Structure):
-    _fields_ = [("id", c_i32), ("cached", c_i32), ("prompt", c_i32), ("gen", c_i32), ("src_base", c_i32)]
+    _fields_ = [("id", c_i32), ("cached", c_i32), ("prompt", c_i32), ("gen", c_i32), ("src_base", c_i32),
+                ("arrival_iter", c_i32), ("arrival_us", c_dbl)]
 
 
 class EngineStats(ctypes.Structure):
@@ -71,7 +73,8 @@ class EngineStats(ctypes.Structure):
                 ("decode_iters", c_i32), ("prefill_groups", c_i32), ("split_changes", c_i32), ("handoffs", c_i32),
                 ("busy_dec_us", c_dbl), ("busy_pf_us", c_dbl), ("bubble_ratio", c_dbl), ("bubble_ratio_dec", c_dbl),
                 ("bubble_ratio_pf", c_dbl), ("tbt_mean_us", c_dbl), ("tbt_max_us", c_dbl), ("ttft_mean_us", c_dbl),
-                ("ttft_max_us", c_dbl)]
+                ("ttft_max_us", c_dbl), ("gap_mean_us", c_dbl), ("gap_max_us", c_dbl), ("graphs", c_i32),
+                ("graph_bytes", c_i64), ("logged_rows", c_i32)]
 
     def as_dict(self):
         return {k: getattr(self, k) for k, _ in self._fields_}
@@ -115,12 +118,14 @@ def lib():
         "mux_stream_read": [c_p, c_sz, c_i32, c_p],
         "mux_run_layer": [c_p, c_i32, c_p, ctypes.POINTER(SideC), ctypes.POINTER(SideC), c_p, c_p],
         "mux_outproj": [c_p, c_p, c_p, c_i32, c_i32, c_i32, c_i32, c_p],
+        "mux_outproj_sms": [c_p, c_p, c_p, c_i32, c_i32, c_i32, c_i32, c_p, c_i32],
         "mux_outproj_pack_w": [c_p, c_p, c_i32, c_i32, c_p],
         "mux_engine_create": [ctypes.POINTER(c_p), c_p, c_p, ctypes.POINTER(EngineDesc)],
         "mux_engine_submit": [c_p, ctypes.POINTER(RequestC), c_i32],
         "mux_engine_run": [c_p, ctypes.POINTER(EngineStats)],
         "mux_engine_request_pages": [c_p, c_i32, ctypes.POINTER(c_i32), c_p, c_i32, ctypes.POINTER(c_i32)],
         "mux_engine_trace": [c_p, c_p, c_i32, ctypes.POINTER(c_i32)],
+        "mux_engine_out_rows": [c_p, c_p, c_i32, ctypes.POINTER(c_i32)],
         "mux_engine_destroy": [c_p],
     }
     for name, args in sig.items():
@@ -356,7 +361,7 @@ def mux_outproj_pack_w(w, stream=None) -> PackedW:
     return PackedW(out, K, N)
 
 
-def mux_outproj(x, w: PackedW, y, stream=None):
+def mux_outproj(x, w: PackedW, y, stream=None, num_sms: int = 0):
     """a7 partial GEMM: y[T][N] = x[T][K] . W[K][N] (bf16 in, fp32 accumulate, y bf16 or fp32);
     W packed by mux_outproj_pack_w."""
     import torch
@@ -365,7 +370,7 @@ def mux_outproj(x, w: PackedW, y, stream=None):
     N = w.N
     assert K == w.K and tuple(y.shape) == (T, N)
     yd = MUX_DTYPE_F32 if y.dtype == torch.float32 else MUX_DTYPE_BF16
-    _check(lib().mux_outproj(_ptr(x), _ptr(w.data), _ptr(y), yd, T, K, N, _stream(stream)))
+    _check(lib().mux_outproj_sms(_ptr(x), _ptr(w.data), _ptr(y), yd, T, K, N, _stream(stream), num_sms))
 
 
 def mux_device_sm_count(device: int = 0) -> int:
@@ -419,9 +424,13 @@ def mux_partition_create(device: int, decode_sms: Sequence[int]) -> Partition:
 
 def make_side(batch: Batch, num_q_heads: int, q, o, k_new=None, v_new=None, lse=None, scale: float = 1.0,
               layer0: int = 0, num_layers: int = 1, append: bool = False, num_splits: int = 0, ws=None,
-              per_layer_inputs: bool = False, w_o=None, y=None, hook=None) -> SideC:
+              per_layer_inputs: bool = False, w_o=None, y=None, hook=None, allreduce=None,
+              attn_events=None) -> SideC:
     """Build a mux_side.  per_layer_inputs: q/k_new/v_new/o/lse carry a leading layer dim
-    and layer i uses slice i (stride = one slice); otherwise every layer reuses the buffers."""
+    and layer i uses slice i (stride = one slice); otherwise every layer reuses the buffers.
+    allreduce: (fn address, comm handle) of the NCCL all-reduce the library enqueues after every
+    layer's out-projection (nccl.Comm.c_allreduce()).  attn_events: 2 * num_layers raw
+    cudaEvent_t handles (EventSet) recorded around every layer's attention."""
     import torch
 
     def stride(t):
@@ -453,8 +462,37 @@ def make_side(batch: Batch, num_q_heads: int, q, o, k_new=None, v_new=None, lse=
         # hook(side, layer_index, stream_handle) -> None; enqueue work on that stream
         cb = LayerHook(lambda user, side, layer, stream: hook(int(side), int(layer), int(stream or 0)))
         s.hook = cb
-    s._keep = (batch, q, o, k_new, v_new, lse, ws, w_o, y, cb)
+    if allreduce is not None:
+        s.ar_fn, s.ar_comm = allreduce
+    ev_arr = None
+    if attn_events is not None:
+        assert len(attn_events) >= 2 * num_layers
+        ev_arr = (c_p * len(attn_events))(*attn_events.handles())
+        s.attn_events = ctypes.cast(ev_arr, c_p)
+    s._keep = (batch, q, o, k_new, v_new, lse, ws, w_o, y, cb, ev_arr, attn_events)
     return s
+
+
+class EventSet:
+    """n timing-enabled CUDA events as raw handles (created through the CUDA runtime torch loaded),
+    for mux_side.attn_events; durations(i) = ms between events 2i and 2i+1 after a sync."""
+
+    def __init__(self, n: int):
+        import torch
+        self.ev = [torch.cuda.Event(enable_timing=True) for _ in range(n)]
+        s = torch.cuda.Stream()
+        for e in self.ev:          # materialise the cudaEvent_t (torch creates it on first record)
+            e.record(s)
+        s.synchronize()
+
+    def __len__(self):
+        return len(self.ev)
+
+    def handles(self):
+        return [int(e.cuda_event) for e in self.ev]
+
+    def durations_ms(self, pairs: int):
+        return [self.ev[2 * i].elapsed_time(self.ev[2 * i + 1]) for i in range(pairs)]
 
 
 def mux_run_layer(part: Partition, split_idx: int, pool: Pool, prefill: Optional[SideC], decode: Optional[SideC],
@@ -473,7 +511,8 @@ class Engine:
     def __init__(self, part: "Partition", pool: Pool, num_q_heads: int, src_q, src_k, src_v, *,
                  scale: float, w_o: "PackedW" = None, max_decode_seqs: int = 256,
                  max_prefill_tokens: int = 16384, fixed_split: int = -2, cost=None, tbt_slo_us: float = 1e30,
-                 fixed_pl: int = 0, handoff: bool = True, keep_pages: bool = False, serialize: bool = False):
+                 fixed_pl: int = 0, handoff: bool = True, keep_pages: bool = False, serialize: bool = False,
+                 use_graphs: bool = False, o_log=None, y_log=None, o_f32: bool = False, overlap: bool = False):
         d = EngineDesc()
         d.num_q_heads, d.scale = num_q_heads, scale
         d.src_q, d.src_k, d.src_v = _ptr(src_q), _ptr(src_k), _ptr(src_v)
@@ -483,7 +522,12 @@ class Engine:
         d.max_decode_seqs, d.max_prefill_tokens = max_decode_seqs, max_prefill_tokens
         d.fixed_split, d.tbt_slo_us, d.fixed_pl = fixed_split, tbt_slo_us, fixed_pl
         d.handoff, d.keep_pages, d.serialize = int(handoff), int(keep_pages), int(serialize)
-        self._keep = [src_q, src_k, src_v, w_o]
+        d.use_graphs, d.o_f32, d.overlap = int(use_graphs), int(o_f32), int(overlap)
+        if o_log is not None:
+            d.o_log, d.log_rows = _ptr(o_log), int(o_log.shape[0])
+            if y_log is not None:
+                d.y_log = _ptr(y_log)
+        self._keep = [src_q, src_k, src_v, w_o, o_log, y_log]
         if cost is not None:
             n = part.n
             dec = np.zeros((n, 3))
@@ -503,7 +547,7 @@ class Engine:
         self.h = h
 
     def submit(self, reqs):
-        """reqs: iterable of (id, cached, prompt, gen, src_base)."""
+        """reqs: iterable of (id, cached, prompt, gen, src_base[, arrival_iter[, arrival_us]])."""
         arr = (RequestC * len(reqs))(*[RequestC(*r) for r in reqs])
         _check(lib().mux_engine_submit(self.h, arr, len(reqs)))
 
@@ -524,6 +568,14 @@ class Engine:
         _check(lib().mux_engine_trace(self.h, None, 0, ctypes.byref(n)))
         out = np.zeros((max(1, n.value), 6), np.int64)
         _check(lib().mux_engine_trace(self.h, out.ctypes.data, n.value, ctypes.byref(n)))
+        return out[:n.value]
+
+    def out_rows(self):
+        """[(request id, absolute position, decode?)] of the rows in o_log / y_log."""
+        n = c_i32()
+        _check(lib().mux_engine_out_rows(self.h, None, 0, ctypes.byref(n)))
+        out = np.zeros((max(1, n.value), 3), np.int32)
+        _check(lib().mux_engine_out_rows(self.h, out.ctypes.data, n.value, ctypes.byref(n)))
         return out[:n.value]
 
     def close(self):

@@ -44,6 +44,12 @@ __global__ void gather_rows_kernel(const uint4* __restrict__ src, uint4* __restr
   }
 }
 
+// %globaltimer into log[*idx + off]: a captured decode iteration writes its stamps to the log
+// slot the host stored in device memory before the replay (a graph's parameters are fixed)
+__global__ void stamp_at_kernel(unsigned long long* log, const int32_t* idx, int off) {
+  log[*idx + off] = dev::globaltimer();
+}
+
 int gather(const void* src, void* dst, const int32_t* idx, int rows, int row_bytes, cudaStream_t st) {
   if (rows <= 0) return MUX_OK;
   const int vec = row_bytes / 16;
@@ -58,7 +64,8 @@ struct Req {
   mux_request r{};
   std::vector<int32_t> pages;
   int ctx = 0;          // tokens in the pool (kv_len after the last append)
-  int gen_left = 0;
+  int gen_launched = 0;  // decode iterations enqueued for it
+  int gen_done = 0;      // ... and completed
   int ttft_log = -1;    // log slot of the end stamp of its last prefill group
   int arrive_log = -1;  // log slot of the end stamp of the decode iteration that met arrival_iter
   bool arrived = false;
@@ -104,7 +111,9 @@ struct mux_engine {
   size_t osz = 2;                      // bytes per attention output element (bf16 / f32)
   // device buffers
   void *dq = nullptr, *dk = nullptr, *dv = nullptr, *do_ = nullptr, *dy = nullptr, *ws = nullptr;
-  int32_t* dfix = nullptr;             // the decode iteration's batch arrays (fixed address: graphs)
+  // f2 graphs: the iteration's batch arrays at a FIXED address, [0] = the log slot of its start
+  // stamp (the end stamp goes to the next slot), then the build_batch layout
+  int32_t* dfix = nullptr;
   size_t ws_bytes = 0;
   // f2: decode-iteration graphs keyed by (split, batch size, split-KV count, pages per split)
   std::map<std::tuple<int, int, int, int>, cudaGraphExec_t> graphs;
@@ -255,12 +264,12 @@ static int engine_alloc(mux_engine* e) {
   MUX_CUDA(cudaMalloc(&e->prev, e->cap_pre * kvrow));
   const size_t nreq = e->reqs.size();
   for (int i = 0; i < 2; ++i) {
-    int rc = slot_reserve(e->dslot[i], 4 * static_cast<size_t>(e->cap_dec) + 8 + tot_pages);
+    int rc = slot_reserve(e->dslot[i], 4 * static_cast<size_t>(e->cap_dec) + 9 + tot_pages);
     if (!rc) rc = slot_reserve(e->pslot[i], 4 * nreq + 8 + tot_pages + e->cap_pf);
     if (!rc) rc = slot_reserve(e->preslot[i], 4 * nreq + 8 + tot_pages + e->cap_pre);
     if (rc) return rc;
   }
-  MUX_CUDA(cudaMalloc(&e->dfix, (4 * static_cast<size_t>(e->cap_dec) + 8 + tot_pages) * 4));
+  if (e->desc.use_graphs) MUX_CUDA(cudaMalloc(&e->dfix, (4 * static_cast<size_t>(e->cap_dec) + 9 + tot_pages) * 4));
   e->log_cap = static_cast<int>(2 * (iters + static_cast<int64_t>(e->NT) * nreq + 64));
   MUX_CUDA(cudaMalloc(&e->log, static_cast<size_t>(e->log_cap) * 8));
   return pool_tmaps(e->pool);   // device-side pool state exists before any graph capture
@@ -329,11 +338,36 @@ int mux_engine_run(mux_engine_t e, mux_engine_stats* st) {
   const int Hq = D.num_q_heads, d = e->d, NT = e->NT, Hkv = e->Hkv;
   const size_t qrow = static_cast<size_t>(Hq) * d * 2, kvrow = static_cast<size_t>(Hkv) * d * 2;
   const int nsplit = mux_partition_count(e->part);
-  std::deque<int> queue;
+  // FCFS in arrival order (arrival_iter, then arrival_us), submission order among equals
+  std::vector<int> order(e->reqs.size());
   for (int i = 0; i < static_cast<int>(e->reqs.size()); ++i) {
-    e->reqs[i].gen_left = e->reqs[i].r.gen;
-    queue.push_back(i);
+    e->reqs[i].gen_launched = e->reqs[i].gen_done = 0;
+    order[i] = i;
   }
+  std::stable_sort(order.begin(), order.end(), [&](int a, int b) {
+    const mux_request &x = e->reqs[a].r, &y = e->reqs[b].r;
+    return x.arrival_iter != y.arrival_iter ? x.arrival_iter < y.arrival_iter : x.arrival_us < y.arrival_us;
+  });
+  std::deque<int> queue(order.begin(), order.end());
+  const auto t_run0 = std::chrono::steady_clock::now();
+  auto elapsed_us = [&]() {
+    return std::chrono::duration<double, std::micro>(std::chrono::steady_clock::now() - t_run0).count();
+  };
+  int dec_done = 0;                    // decode iterations completed (arrival_iter clock)
+  std::vector<int> iter_end_log;       // log slot of each completed iteration's end stamp
+  const size_t orow = static_cast<size_t>(Hq) * d * e->osz;
+  // output log: rows [row0, row0 + rows) of `o` (and `y`) appended if they fit
+  auto log_out = [&](const void* o, const void* y, int rows, cudaStream_t st) -> int {
+    if (!D.log_rows || e->log_rows_used + rows > D.log_rows) return MUX_OK;
+    const size_t r0 = static_cast<size_t>(e->log_rows_used);
+    MUX_CUDA(cudaMemcpyAsync(static_cast<uint8_t*>(D.o_log) + r0 * orow, o, rows * orow, cudaMemcpyDeviceToDevice, st));
+    if (D.w_o) {
+      const size_t yrow = static_cast<size_t>(D.hidden) * 2;
+      MUX_CUDA(cudaMemcpyAsync(static_cast<uint8_t*>(D.y_log) + r0 * yrow, y, rows * yrow, cudaMemcpyDeviceToDevice, st));
+    }
+    e->log_rows_used += rows;
+    return MUX_OK;
+  };
   std::vector<int> decode, ready;
   std::deque<Group> pf_out;
   struct Job {
@@ -344,9 +378,16 @@ int mux_engine_run(mux_engine_t e, mux_engine_stats* st) {
     double sum_n2 = 0, sum_nr = 0, sum_n = 0;
   } job;
   int job_buf = 0, dslot_i = 0, pslot_i = 0, preslot_i = 0;
-  bool dec_inflight = false;
-  cudaEvent_t dec_ev = nullptr;
-  std::vector<int> dec_members;
+  // decode iterations in flight, oldest first: 1 (launch after completion) or, with
+  // desc.overlap, 2 (the next iteration is enqueued behind the running one: no device gap)
+  struct Iter {
+    cudaEvent_t ev;
+    std::vector<int> members;
+    int li;
+  };
+  std::deque<Iter> dec_q;
+  const size_t depth = D.overlap ? 2 : 1;
+  cudaEvent_t last_dec_ev = nullptr;
   int cur_split = D.fixed_split >= -1 ? D.fixed_split : -1;
   int last_dec_split = -3, last_pf_split = -3;
   cudaEvent_t last_pf_ev = nullptr;
@@ -392,17 +433,17 @@ int mux_engine_run(mux_engine_t e, mux_engine_stats* st) {
     // ---- 1. decode iteration completed: tokens "returned", finished requests retire
     // event_done: cudaSuccess -> true, cudaErrorNotReady -> false, anything else (a sticky fault of
     // a kernel, e.g. cudaErrorIllegalAddress) ends the run with MUX_ERR_CUDA instead of polling forever
-    if (dec_inflight && (rc = event_done(dec_ev, &done)) != MUX_OK) return rc;
-    if (dec_inflight && done) {
-      dec_inflight = false;
+    while (!dec_q.empty()) {
+      if ((rc = event_done(dec_q.front().ev, &done)) != MUX_OK) return rc;
+      if (!done) break;
       did = true;
-      std::vector<int> keep;
-      for (int i : dec_members) {
+      ++dec_done;
+      iter_end_log.push_back(dec_q.front().li + 1);
+      for (int i : dec_q.front().members) {
         Req& r = e->reqs[i];
-        if (--r.gen_left == 0) release(r);
-        else keep.push_back(i);
+        if (++r.gen_done == r.r.gen) release(r);
       }
-      decode = keep;
+      dec_q.pop_front();
     }
     // ---- 2. prefill groups completed (in order); a finished prefill is ready to merge
     while (!pf_out.empty()) {
@@ -414,12 +455,16 @@ int mux_engine_run(mux_engine_t e, mux_engine_stats* st) {
       if (g.last)
         for (int i : g.reqs) {
           Req& r = e->reqs[i];
-          if (r.gen_left > 0) ready.push_back(i);
+          if (r.r.gen > 0) ready.push_back(i);
           else release(r);
         }
     }
     // ---- 3. next decode iteration (launched first)
-    if (!dec_inflight) {
+    if (dec_q.size() < depth) {
+      // requests whose last iteration is already enqueued leave the batch
+      decode.erase(std::remove_if(decode.begin(), decode.end(),
+                                  [&](int i) { return e->reqs[i].gen_launched >= e->reqs[i].r.gen; }),
+                   decode.end());
       while (!ready.empty() && static_cast<int>(decode.size()) < D.max_decode_seqs) {
         decode.push_back(ready.front());
         ready.erase(ready.begin());
@@ -434,10 +479,13 @@ int mux_engine_run(mux_engine_t e, mux_engine_stats* st) {
         cudaStream_t ds, ps;
         int dsms, psms;
         if ((rc = streams(sp, &ds, &ps, &dsms, &psms))) return rc;
+        // the iteration reuses the previous one's buffers: order it after it across a split change
+        if (last_dec_ev && sp != last_dec_split) MUX_CUDA(cudaStreamWaitEvent(ds, last_dec_ev, 0));
         std::vector<Req*> rs;
         std::vector<int> nn, kv, p0;
         for (int i : decode) {
           Req& r = e->reqs[i];
+          ++r.gen_launched;
           if (r.ctx % kPage == 0) {  // the new token opens a page
             int32_t id;
             if ((rc = mux_pool_alloc_pages(e->pool, 1, &id))) return rc;
@@ -449,17 +497,31 @@ int mux_engine_run(mux_engine_t e, mux_engine_stats* st) {
           nn.push_back(1);
           kv.push_back(r.ctx);
         }
+        int li;
+        if ((rc = log_pair(e, &li))) return rc;
+        // batch arrays: the slot's own device copy, or (graphs) the fixed buffer every captured
+        // iteration reads, with [0] = the log slot of its end stamp (stream order keeps a running
+        // iteration's reads ahead of the next upload)
         Slot& s = e->dslot[dslot_i];
         dslot_i ^= 1;
         if ((rc = slot_acquire(s))) return rc;
-        Built bt = build_batch(s, rs, nn, kv, p0, D.src_rows);
-        MUX_CUDA(cudaMemcpyAsync(s.d, s.h, bt.n * 4, cudaMemcpyHostToDevice, ds));
+        const int off = D.use_graphs ? 1 : 0;
+        int32_t* dev = D.use_graphs ? e->dfix : s.d;
+        Slot view = s;
+        view.h = s.h + off;
+        Built bt = build_batch(view, rs, nn, kv, p0, D.src_rows, dev + off);
+        s.h[0] = D.use_graphs ? li : s.h[0];
+        launch_stamp(e->log + li, ds);   // the iteration starts with its batch upload
+        MUX_CUDA(cudaMemcpyAsync(dev, s.h, (bt.n + off) * 4, cudaMemcpyHostToDevice, ds));
         MUX_CUDA(cudaEventRecord(s.done, ds));
         s.used = true;
         const int B = bt.rows;
-        if ((rc = gather(D.src_q, e->dq, bt.d_idx, B, static_cast<int>(qrow), ds))) return rc;
-        if ((rc = gather(D.src_k, e->dk, bt.d_idx, B, static_cast<int>(kvrow), ds))) return rc;
-        if ((rc = gather(D.src_v, e->dv, bt.d_idx, B, static_cast<int>(kvrow), ds))) return rc;
+        auto gathers = [&]() -> int {
+          int r2;
+          if ((r2 = gather(D.src_q, e->dq, bt.d_idx, B, static_cast<int>(qrow), ds))) return r2;
+          if ((r2 = gather(D.src_k, e->dk, bt.d_idx, B, static_cast<int>(kvrow), ds))) return r2;
+          return gather(D.src_v, e->dv, bt.d_idx, B, static_cast<int>(kvrow), ds);
+        };
         mux_side side{};
         side.batch = &bt.b;
         side.num_q_heads = Hq;
@@ -467,7 +529,7 @@ int mux_engine_run(mux_engine_t e, mux_engine_stats* st) {
         side.k_new = e->dk;
         side.v_new = e->dv;
         side.o = e->do_;
-        side.o_dtype = MUX_DTYPE_BF16;
+        side.o_dtype = e->osz == 4 ? MUX_DTYPE_F32 : MUX_DTYPE_BF16;
         side.scale = D.scale;
         side.layer0 = 0;
         side.num_layers = NT;
@@ -481,14 +543,58 @@ int mux_engine_run(mux_engine_t e, mux_engine_stats* st) {
           side.hidden = D.hidden;
           side.y_dtype = MUX_DTYPE_BF16;
         }
-        int li;
-        if ((rc = log_pair(e, &li))) return rc;
-        if ((rc = run_side(e->pool, &side, true, dsms, ds, e->log + li, e->log + li + 1))) return rc;
+        if (!D.use_graphs) {
+          if ((rc = gathers())) return rc;
+          if ((rc = run_side(e->pool, &side, true, dsms, ds, nullptr, e->log + li + 1))) return rc;
+        } else {
+          // f2: the whole iteration is one graph launch.  Its launch shapes are fixed by
+          // (split, B, split-KV count, pages per split); everything else it reads from device memory.
+          const int S = mux_decode_num_splits(B, Hkv, d, bt.b.h_kv_len, bt.b.max_kv, dsms);
+          const int maxp = (bt.b.max_kv + kPage - 1) / kPage;
+          const int pps = std::max(1, (maxp + S - 1) / S);
+          side.num_splits = S;
+          const auto key = std::make_tuple(sp, B, S, pps);
+          auto it = e->graphs.find(key);
+          if (it == e->graphs.end()) {
+            MUX_CUDA(cudaStreamBeginCapture(ds, cudaStreamCaptureModeThreadLocal));
+            int r2 = gathers();
+            if (!r2) r2 = run_side(e->pool, &side, true, dsms, ds, nullptr, nullptr);
+            if (!r2) stamp_at_kernel<<<1, 1, 0, ds>>>(e->log, e->dfix, 1);   // end stamp: log[li + 1]
+            cudaGraph_t g = nullptr;
+            const cudaError_t ce = cudaStreamEndCapture(ds, &g);
+            if (r2) {
+              if (g) cudaGraphDestroy(g);
+              return r2;
+            }
+            MUX_CUDA(ce);
+            size_t f0 = 0, f1 = 0, tot = 0;
+            MUX_CUDA(cudaMemGetInfo(&f0, &tot));
+            cudaGraphExec_t x = nullptr;
+            const cudaError_t ie = cudaGraphInstantiate(&x, g, 0);
+            cudaGraphDestroy(g);
+            MUX_CUDA(ie);
+            MUX_CUDA(cudaGraphUpload(x, ds));
+            MUX_CUDA(cudaMemGetInfo(&f1, &tot));
+            e->graph_bytes += static_cast<int64_t>(f0) - static_cast<int64_t>(f1);
+            it = e->graphs.emplace(key, x).first;
+          }
+          MUX_CUDA(cudaGraphLaunch(it->second, ds));
+        }
+        if (D.log_rows && e->log_rows_used + B <= D.log_rows) {
+          for (int k = 0; k < B; ++k) {
+            const Req& r = *rs[k];
+            e->out_rows.insert(e->out_rows.end(), {r.r.id, p0[k], 1});
+          }
+          if ((rc = log_out(e->do_, e->dy, B, ds))) return rc;
+        }
         e->iv.push_back({0, li, sp, B});
-        if ((rc = new_event(e, &dec_ev))) return rc;
-        MUX_CUDA(cudaEventRecord(dec_ev, ds));
-        dec_members = decode;
-        dec_inflight = true;
+        Iter it{};
+        if ((rc = new_event(e, &it.ev))) return rc;
+        MUX_CUDA(cudaEventRecord(it.ev, ds));
+        it.members = decode;
+        it.li = li;
+        dec_q.push_back(it);
+        last_dec_ev = it.ev;
         last_dec_split = sp;
         dc_tokens += B;
         ++iters;
@@ -496,11 +602,24 @@ int mux_engine_run(mux_engine_t e, mux_engine_stats* st) {
       }
     }
     // ---- 4. admit the next prefill batch (FCFS, up to max_prefill_tokens new tokens)
-    if (!job.active && !queue.empty()) {
+    // arrival gate: decode iterations completed and host time since the start; a request waiting
+    // for an iteration count no decode work can reach is admitted when the engine would idle
+    const bool no_decode_work = decode.empty() && ready.empty() && dec_q.empty();
+    auto admissible = [&](int i) {
+      const mux_request& r = e->reqs[i].r;
+      if (elapsed_us() < r.arrival_us) return false;
+      return dec_done >= r.arrival_iter || (no_decode_work && pf_out.empty() && !job.active);
+    };
+    if (!job.active && !queue.empty() && admissible(queue.front())) {
       job = Job();
       int tok = 0;
-      while (!queue.empty() && (job.reqs.empty() || tok + e->reqs[queue.front()].r.prompt <= D.max_prefill_tokens)) {
-        tok += e->reqs[queue.front()].r.prompt;
+      while (!queue.empty() && admissible(queue.front()) &&
+             (job.reqs.empty() || tok + e->reqs[queue.front()].r.prompt <= D.max_prefill_tokens)) {
+        Req& r = e->reqs[queue.front()];
+        const int k = std::min(r.r.arrival_iter, dec_done);
+        r.arrive_log = k > 0 ? iter_end_log[k - 1] : -1;
+        r.arrived = true;
+        tok += r.r.prompt;
         job.reqs.push_back(queue.front());
         queue.pop_front();
       }
@@ -508,7 +627,7 @@ int mux_engine_run(mux_engine_t e, mux_engine_stats* st) {
       job.buf = job_buf;
       job_buf ^= 1;
       // target stream of the prep work: that of the first group
-      const int sp = (decode.empty() && ready.empty() && !dec_inflight) ? -1 : cur_split;
+      const int sp = (decode.empty() && ready.empty() && dec_q.empty()) ? -1 : cur_split;
       cudaStream_t ds, ps;
       int dsms, psms;
       if ((rc = streams(sp, &ds, &ps, &dsms, &psms))) return rc;
@@ -572,7 +691,7 @@ int mux_engine_run(mux_engine_t e, mux_engine_stats* st) {
     }
     // ---- 5. keep up to two prefill groups of N_PL layers queued (layer-wise prefill)
     if (job.active && job.layers_done < NT && pf_out.size() < 2) {
-      const bool dec_idle = decode.empty() && ready.empty() && !dec_inflight;
+      const bool dec_idle = decode.empty() && ready.empty() && dec_q.empty();
       int sp = cur_split;
       if (dec_idle && (D.handoff || !decode_seen)) {
         if (sp != -1 && decode_seen && last_pf_split != -1) ++handoffs;
@@ -601,7 +720,7 @@ int mux_engine_run(mux_engine_t e, mux_engine_stats* st) {
       side.k_new = e->pk[job.buf];
       side.v_new = e->pv[job.buf];
       side.o = e->po[job.buf];
-      side.o_dtype = MUX_DTYPE_BF16;
+      side.o_dtype = e->osz == 4 ? MUX_DTYPE_F32 : MUX_DTYPE_BF16;
       side.scale = D.scale;
       side.layer0 = job.layers_done;
       side.num_layers = npl;
@@ -625,6 +744,14 @@ int mux_engine_run(mux_engine_t e, mux_engine_stats* st) {
         g.reqs = job.reqs;
         for (int i : job.reqs) e->reqs[i].ttft_log = li + 1;
         job.active = false;
+        const int T = job.batch.rows;
+        if (D.log_rows && e->log_rows_used + T <= D.log_rows) {
+          for (int i : job.reqs) {
+            const Req& r = e->reqs[i];
+            for (int t = 0; t < r.r.prompt; ++t) e->out_rows.insert(e->out_rows.end(), {r.r.id, r.r.cached + t, 0});
+          }
+          if ((rc = log_out(e->po[job.buf], e->py[job.buf], T, ps))) return rc;
+        }
       }
       pf_out.push_back(g);
       last_pf_ev = g.ev;
@@ -633,7 +760,7 @@ int mux_engine_run(mux_engine_t e, mux_engine_stats* st) {
       did = true;
     }
     // ---- 6. done?
-    if (!dec_inflight && pf_out.empty() && !job.active && queue.empty() && ready.empty() && decode.empty()) break;
+    if (dec_q.empty() && pf_out.empty() && !job.active && queue.empty() && ready.empty() && decode.empty()) break;
     if (!did) std::this_thread::yield();
   }
   MUX_CUDA(cudaDeviceSynchronize());
@@ -698,11 +825,30 @@ int mux_engine_run(mux_engine_t e, mux_engine_stats* st) {
     prev_end = lg[v.log + 1];
   }
   S.tbt_mean_us = tn ? tsum / tn : 0.0;
+  // decode-side launch gap: idle device time between consecutive iterations
+  prev_end = 0;
+  double gsum = 0;
+  int gn = 0;
+  for (auto& v : e->iv) {
+    if (v.side != 0) continue;
+    if (prev_end) {
+      const double t = lg[v.log] > prev_end ? (lg[v.log] - prev_end) * 1e-3 : 0.0;
+      gsum += t;
+      ++gn;
+      S.gap_max_us = std::max(S.gap_max_us, t);
+    }
+    prev_end = lg[v.log + 1];
+  }
+  S.gap_mean_us = gn ? gsum / gn : 0.0;
+  S.graphs = static_cast<int32_t>(e->graphs.size());
+  S.graph_bytes = e->graph_bytes;
+  S.logged_rows = e->log_rows_used;
   double fsum = 0;
   int fn = 0;
   for (auto& r : e->reqs)
     if (r.ttft_log >= 0) {
-      const double t = (lg[r.ttft_log] - t_first) * 1e-3;
+      const unsigned long long a = r.arrive_log >= 0 ? lg[r.arrive_log] : t_first;
+      const double t = lg[r.ttft_log] > a ? (lg[r.ttft_log] - a) * 1e-3 : 0.0;
       fsum += t;
       ++fn;
       S.ttft_max_us = std::max(S.ttft_max_us, t);
@@ -747,9 +893,21 @@ int mux_engine_trace(mux_engine_t e, int64_t* out, int32_t cap, int32_t* n) {
   return MUX_OK;
 }
 
+int mux_engine_out_rows(mux_engine_t e, int32_t* out, int32_t cap, int32_t* n) {
+  if (!e || !n) return fail(MUX_ERR_INVALID_ARG, "bad argument");
+  const int rows = static_cast<int>(e->out_rows.size() / 3);
+  if (out)
+    for (int i = 0; i < rows && i < cap; ++i)
+      for (int j = 0; j < 3; ++j) out[3 * i + j] = e->out_rows[3 * i + j];
+  *n = rows;
+  return MUX_OK;
+}
+
 int mux_engine_destroy(mux_engine_t e) {
   if (!e) return MUX_OK;
   cudaDeviceSynchronize();
+  for (auto& kv : e->graphs) cudaGraphExecDestroy(kv.second);
+  if (e->dfix) cudaFree(e->dfix);
   for (void* p : {e->dq, e->dk, e->dv, e->do_, e->dy, e->ws, e->prek, e->prev})
     if (p) cudaFree(p);
   for (int i = 0; i < 2; ++i) {

@@ -581,3 +581,8 @@ extern "C" int mux_outproj(const void* x, const void* w, void* y, int32_t y_dtyp
                            mux_stream_t stream) {
   return mux::outproj_launch(x, w, y, y_dtype, T, K, N, stream, 0);
 }
+
+extern "C" int mux_outproj_sms(const void* x, const void* w, void* y, int32_t y_dtype, int32_t T, int32_t K,
+                               int32_t N, mux_stream_t stream, int32_t num_sms) {
+  return mux::outproj_launch(x, w, y, y_dtype, T, K, N, stream, num_sms);
+}

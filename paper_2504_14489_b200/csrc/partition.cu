@@ -169,6 +169,14 @@ int run_side(mux_pool_t pool, const mux_side* s, bool decode, int sms, cudaStrea
              unsigned long long* t1) {
   if (s->w_o && (s->o_dtype != MUX_DTYPE_BF16 || !s->y || s->hidden < 1))
     return fail(MUX_ERR_INVALID_ARG, "out-projection needs bf16 o, y and hidden >= 1");
+  if (s->ar_fn && (!s->w_o || !s->ar_comm || s->y_dtype != MUX_DTYPE_BF16))
+    return fail(MUX_ERR_INVALID_ARG, "all-reduce needs w_o, a bf16 y and ar_comm");
+  using nccl_allreduce_t = int (*)(const void*, void*, size_t, int, int, void*, cudaStream_t);
+  auto ar = reinterpret_cast<nccl_allreduce_t>(s->ar_fn);
+  auto ev = [&](int i, int which) -> int {
+    if (s->attn_events) MUX_CUDA(cudaEventRecord(static_cast<cudaEvent_t>(s->attn_events[2 * i + which]), st));
+    return MUX_OK;
+  };
   if (t0) stamp_kernel<<<1, 1, 0, st>>>(t0);
   const int nl = pool->desc.num_layers;
   int splits = 1;
@@ -190,6 +198,7 @@ int run_side(mux_pool_t pool, const mux_side* s, bool decode, int sms, cudaStrea
     }
     void* o = const_cast<void*>(at(s->o, s->o_stride));
     float* lse = static_cast<float*>(const_cast<void*>(at(s->lse, s->lse_stride)));
+    if ((rc = ev(i, 0))) return rc;
     if (decode)
       rc = mux_decode_attn(pool, layer, s->batch, s->num_q_heads, at(s->q, s->q_stride), o, s->o_dtype, lse,
                            s->scale, splits, s->ws, s->ws_bytes, reinterpret_cast<mux_stream_t>(st));
@@ -197,11 +206,17 @@ int run_side(mux_pool_t pool, const mux_side* s, bool decode, int sms, cudaStrea
       rc = mux_prefill_attn(pool, layer, s->batch, s->num_q_heads, at(s->q, s->q_stride), o, s->o_dtype, lse,
                             s->scale, reinterpret_cast<mux_stream_t>(st));
     if (rc) return rc;
+    if ((rc = ev(i, 1))) return rc;
     if (s->w_o) {
-      rc = outproj_launch(o, at(s->w_o, s->w_stride), const_cast<void*>(at(s->y, s->y_stride)), s->y_dtype,
-                          s->batch->total_q, s->num_q_heads * pool->desc.head_dim, s->hidden,
-                          reinterpret_cast<mux_stream_t>(st), sms);
+      void* y = const_cast<void*>(at(s->y, s->y_stride));
+      rc = outproj_launch(o, at(s->w_o, s->w_stride), y, s->y_dtype, s->batch->total_q,
+                          s->num_q_heads * pool->desc.head_dim, s->hidden, reinterpret_cast<mux_stream_t>(st), sms);
       if (rc) return rc;
+      if (ar) {
+        const int nrc = ar(y, y, static_cast<size_t>(s->batch->total_q) * s->hidden, 9 /* ncclBfloat16 */,
+                           0 /* ncclSum */, s->ar_comm, st);
+        if (nrc) return fail(MUX_ERR_CUDA, "ncclAllReduce of the out-projection failed (NCCL error " + std::to_string(nrc) + ")");
+      }
     }
     if (s->hook) s->hook(s->hook_user, decode ? 0 : 1, i, reinterpret_cast<mux_stream_t>(st));
   }

@@ -89,6 +89,11 @@ class Comm:
         _check(lib().ncclAllReduce(t.data_ptr(), t.data_ptr(), t.numel(), dt, NCCL_SUM, self.comm, stream),
                "ncclAllReduce")
 
+    def c_allreduce(self):
+        """(ncclAllReduce address, comm) for mux_side.ar_fn / ar_comm: the library enqueues each
+        layer's all-reduce from C on the side's stream (no Python in the layer loop)."""
+        return ctypes.cast(lib().ncclAllReduce, ctypes.c_void_p).value, self.comm.value
+
     def close(self):
         if self.comm:
             lib().ncclCommDestroy(self.comm)
