@@ -244,6 +244,14 @@ typedef struct {
   void* const* attn_events;
 } mux_side;
 
+/* Host-only dry run of a side's collective schedule (no GPU needed): for each layer i the side
+ * would process, in enqueue order, out[2*i] = pool layer (layer0 + i) % pool_layers and
+ * out[2*i+1] = element count of the all-reduce run_side enqueues after it (total_q * hidden when
+ * ar_fn is set, else 0).  NCCL needs every rank to issue the same collectives in the same order
+ * on a communicator; multi-rank callers compare these plans across ranks (tests/test_dist_gloo.py).
+ * *n = num_layers; at most cap entries written. */
+int mux_side_plan(const mux_side* side, int32_t pool_layers, int64_t* out, int32_t cap, int32_t* n);
+
 /* device timestamps (%globaltimer, ns) written by 1-thread stamp kernels on each side */
 typedef struct {
   uint64_t dec_start_ns, dec_end_ns, pf_start_ns, pf_end_ns;

@@ -120,6 +120,7 @@ def lib():
         "mux_outproj": [c_p, c_p, c_p, c_i32, c_i32, c_i32, c_i32, c_p],
         "mux_outproj_sms": [c_p, c_p, c_p, c_i32, c_i32, c_i32, c_i32, c_p, c_i32],
         "mux_outproj_pack_w": [c_p, c_p, c_i32, c_i32, c_p],
+        "mux_side_plan": [ctypes.POINTER(SideC), c_i32, c_p, c_i32, ctypes.POINTER(c_i32)],
         "mux_engine_create": [ctypes.POINTER(c_p), c_p, c_p, ctypes.POINTER(EngineDesc)],
         "mux_engine_submit": [c_p, ctypes.POINTER(RequestC), c_i32],
         "mux_engine_run": [c_p, ctypes.POINTER(EngineStats)],
@@ -471,6 +472,15 @@ def make_side(batch: Batch, num_q_heads: int, q, o, k_new=None, v_new=None, lse=
         s.attn_events = ctypes.cast(ev_arr, c_p)
     s._keep = (batch, q, o, k_new, v_new, lse, ws, w_o, y, cb, ev_arr, attn_events)
     return s
+
+
+def mux_side_plan(side: SideC, pool_layers: int) -> np.ndarray:
+    """[(pool layer, all-reduce elements)] in the order libmux would enqueue them (host only)."""
+    n = c_i32()
+    _check(lib().mux_side_plan(ctypes.byref(side), pool_layers, None, 0, ctypes.byref(n)))
+    out = np.zeros((max(1, n.value), 2), np.int64)
+    _check(lib().mux_side_plan(ctypes.byref(side), pool_layers, out.ctypes.data, n.value, ctypes.byref(n)))
+    return out[:n.value]
 
 
 class EventSet:

@@ -34,6 +34,10 @@
 
 #include "pool.h"
 
+#ifndef MUX_DEC_EVICT_FIRST
+#define MUX_DEC_EVICT_FIRST 1
+#endif
+
 namespace mux {
 namespace {
 
@@ -189,6 +193,11 @@ __global__ void __launch_bounds__(DecodeCfg<NT>::kThreads, DecodeCfg<NT>::kCtasP
     uint64_t* empty = is_v ? vempty : kempty;
     uint8_t* ring = smem + (is_v ? L::kVOff : 0);
     if (lane == 0) dev::tma_prefetch(map);
+#if MUX_DEC_EVICT_FIRST
+    // K/V pages are read once per layer: evict-first keeps them from displacing the co-running
+    // prefill's re-read K/V tiles in L2 (SM-partitioned sides still share the 126 MB L2)
+    const uint64_t pol = dev::l2_evict_first();
+#endif
     int ids = 0;
     for (int i = 0; i < n_my; ++i) {
       if ((i & 31) == 0) ids = (pg0 + i + lane < pg1) ? __ldg(ptab + pg0 + i + lane) : 0;
@@ -197,7 +206,11 @@ __global__ void __launch_bounds__(DecodeCfg<NT>::kThreads, DecodeCfg<NT>::kCtasP
       if (lane == 0) {
         if (i >= STAGES) dev::mbar_wait(&empty[s], ((i / STAGES) - 1) & 1);
         dev::mbar_expect_tx(&full[s], L::kStageBytes);
+#if MUX_DEC_EVICT_FIRST
+        dev::tma_load_5d_hint(ring + s * L::kStageBytes, map, &full[s], 0, 0, 0, grp * HG, p.page_row0 + page, pol);
+#else
         dev::tma_load_5d(ring + s * L::kStageBytes, map, &full[s], 0, 0, 0, grp * HG, p.page_row0 + page);
+#endif
       }
     }
   } else {

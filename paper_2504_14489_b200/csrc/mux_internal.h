@@ -66,6 +66,8 @@ int validate_batch(const mux_batch* b, bool need_decode_shape);
 
 // partition.cu: enqueue one side's layers (append + attention (+ combine) + out-projection +
 // hook per layer) on `st`; t0/t1: optional %globaltimer stamps before / after
+// elements of the all-reduce run_side enqueues after each layer (0 = none)
+int64_t side_allreduce_count(const mux_side* s);
 int run_side(mux_pool_t pool, const mux_side* s, bool decode, int sms, cudaStream_t st, unsigned long long* t0,
              unsigned long long* t1);
 void launch_stamp(unsigned long long* dst, cudaStream_t st);
@@ -174,6 +176,27 @@ __device__ __forceinline__ void tma_load_5d(void* dst, const CUtensorMap* map, u
       "cp.async.bulk.tensor.5d.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
       " [%0], [%1, {%2, %3, %4, %5, %6}], [%7];" ::"r"(smem_u32(dst)),
       "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(c2), "r"(c3), "r"(c4), "r"(smem_u32(bar))
+      : "memory");
+}
+// L2 cache policies for TMA loads: streamed-once data (decode K/V pages) evict-first so it does
+// not push the co-running prefill's re-read K/V tiles out of L2; re-read data evict-last
+__device__ __forceinline__ uint64_t l2_evict_first() {
+  uint64_t p;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+__device__ __forceinline__ uint64_t l2_evict_last() {
+  uint64_t p;
+  asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+__device__ __forceinline__ void tma_load_5d_hint(void* dst, const CUtensorMap* map, uint64_t* bar, int c0, int c1,
+                                                 int c2, int c3, int c4, uint64_t policy) {
+  asm volatile(
+      "cp.async.bulk.tensor.5d.shared::cluster.global.tile.mbarrier::complete_tx::bytes.L2::cache_hint"
+      " [%0], [%1, {%2, %3, %4, %5, %6}], [%7], %8;" ::"r"(smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(c2), "r"(c3), "r"(c4), "r"(smem_u32(bar)),
+      "l"(policy)
       : "memory");
 }
 // ---- CTA pair (cluster of 2, tcgen05 cta_group::2) helpers

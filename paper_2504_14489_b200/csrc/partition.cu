@@ -163,6 +163,11 @@ int mux_partition_memory(mux_part_t p, int64_t* bytes) {
 }  // extern "C"
 
 namespace mux {
+// elements of the all-reduce run_side enqueues after each layer's out-projection (0 = none)
+int64_t side_allreduce_count(const mux_side* s) {
+  return (s->ar_fn && s->w_o) ? static_cast<int64_t>(s->batch->total_q) * s->hidden : 0;
+}
+
 void launch_stamp(unsigned long long* dst, cudaStream_t st) { stamp_kernel<<<1, 1, 0, st>>>(dst); }
 
 int run_side(mux_pool_t pool, const mux_side* s, bool decode, int sms, cudaStream_t st, unsigned long long* t0,
@@ -213,7 +218,7 @@ int run_side(mux_pool_t pool, const mux_side* s, bool decode, int sms, cudaStrea
                           s->num_q_heads * pool->desc.head_dim, s->hidden, reinterpret_cast<mux_stream_t>(st), sms);
       if (rc) return rc;
       if (ar) {
-        const int nrc = ar(y, y, static_cast<size_t>(s->batch->total_q) * s->hidden, 9 /* ncclBfloat16 */,
+        const int nrc = ar(y, y, static_cast<size_t>(side_allreduce_count(s)), 9 /* ncclBfloat16 */,
                            0 /* ncclSum */, s->ar_comm, st);
         if (nrc) return fail(MUX_ERR_CUDA, "ncclAllReduce of the out-projection failed (NCCL error " + std::to_string(nrc) + ")");
       }
@@ -227,6 +232,17 @@ int run_side(mux_pool_t pool, const mux_side* s, bool decode, int sms, cudaStrea
 }  // namespace mux
 
 extern "C" {
+
+int mux_side_plan(const mux_side* s, int32_t pool_layers, int64_t* out, int32_t cap, int32_t* n) {
+  if (!s || !s->batch || !n || pool_layers < 1 || s->num_layers < 0 || s->layer0 < 0)
+    return fail(MUX_ERR_INVALID_ARG, "mux_side_plan: bad argument");
+  for (int i = 0; i < s->num_layers && out && i < cap; ++i) {
+    out[2 * i] = (s->layer0 + i) % pool_layers;
+    out[2 * i + 1] = mux::side_allreduce_count(s);
+  }
+  *n = s->num_layers;
+  return MUX_OK;
+}
 
 int mux_run_layer(mux_part_t part, int32_t split_idx, mux_pool_t pool, const mux_side* prefill,
                   const mux_side* decode, mux_side_times* times, mux_stream_t join_stream) {

@@ -1,4 +1,4 @@
-"""One multiplexed bench step (cfg2, fixed split, 1 decode iteration) for ncu launch lists."""
+"""One multiplexed bench step (cfg2, fixed split, DC_LAYERS decode layers) for ncu launch lists."""
 import os, sys
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import torch
@@ -9,7 +9,7 @@ split = int(os.environ.get("SPLIT", 0))
 wl = bench.Workload(2, 0, 1)
 part = mux.Partition(0, mux.mux_partition_configs(mux.mux_device_sm_count(0), 16, 12))
 dsms = part.query(split)[0]
-pf, dc, ns = wl.sides(dsms, 1)
+pf, dc, ns = wl.sides(dsms, int(os.environ.get("DC_LAYERS", 22)))
 torch.cuda.synchronize()
 for _ in range(int(os.environ.get("STEPS", 1))):
     mux.mux_run_layer(part, split, wl.pool, pf, dc, None)

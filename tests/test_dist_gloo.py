@@ -116,3 +116,62 @@ def test_nccl_unique_id_broadcast_keeps_binary_bytes():
     for p in ps:
         p.join(timeout=60)
     assert res == [True, True]
+
+
+def _plan_worker(rank, world, port, q):
+    """Each rank builds ITS shard of the cfg4 step's two sides (Hq/world q heads, hidden 8192,
+    C-side all-reduce set) for 3 steps of the layer-rotating decode side, asks libmux (host dry
+    run, mux_side_plan) for the collective schedule it would enqueue, and all-gathers it."""
+    import torch
+    import torch.distributed as dist
+    import paper_2504_14489_b200 as mux
+    import synth
+    from synth import indptr
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        c = synth.get_config(4)
+        S = c.shapes
+        Hq = S.Hq // world
+        NT = S.n_layers_model
+        D = torch.tensor([37 if rank == 0 else 0])
+        dist.broadcast(D, 0)                     # rank 0 decides the decode layers (as bench.py)
+        D = int(D.item())
+        plans = {}
+        for name, spec in (("pf", c.prefill), ("dc", c.decode)):
+            pages = [(l + 15) // 16 for l in spec.L]
+            pind = np.concatenate([[0], np.cumsum(pages)]).astype(np.int32)
+            b = mux.Batch(indptr(spec.n), spec.L, pind, np.arange(pind[-1], dtype=np.int32), device="cpu")
+            x = torch.zeros((spec.total_new, Hq, S.d), dtype=torch.bfloat16)
+            y = torch.zeros((spec.total_new, S.hidden), dtype=torch.bfloat16)
+            w = mux.PackedW(torch.zeros((1, 16), dtype=torch.uint8), Hq * S.d, S.hidden)
+            for k in range(3):
+                l0, nl = (0, NT) if name == "pf" else ((k * D) % NT, D)
+                side = mux.make_side(b, Hq, x, x, k_new=x, v_new=x, layer0=l0, num_layers=nl, append=True,
+                                     w_o=w, y=y, allreduce=(0x1, 0x1))
+                plans[(name, k)] = mux.mux_side_plan(side, NT).tolist()
+        allp = [None] * world
+        dist.all_gather_object(allp, plans)
+        if rank == 0:
+            q.put(allp)
+    finally:
+        dist.destroy_process_group()
+
+
+def test_collective_order_identical_across_ranks():
+    """NCCL needs every rank to issue the same all-reduces in the same order on each side's
+    communicator: the per-side schedules libmux would enqueue (layer order, element
+    counts) for three steps of the sharded cfg4 workload are identical on both gloo ranks."""
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    ps = [ctx.Process(target=_plan_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in ps:
+        p.start()
+    allp = q.get(timeout=120)
+    for p in ps:
+        p.join(timeout=60)
+    assert allp[0] == allp[1]
+    pf, dc = allp[0][("pf", 0)], allp[0][("dc", 1)]
+    assert [l for l, _ in pf] == list(range(80)) and all(n == 8192 * 8192 for _, n in pf)
+    assert [l for l, _ in dc] == [(37 + i) % 80 for i in range(37)] and all(n == 64 * 8192 for _, n in dc)
