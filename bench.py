@@ -642,13 +642,13 @@ def main():
     dc_attn_ms = np.concatenate([e.durations_ms(D) for e in ev_dc])
     bub = bubble_stats(tt)
     hot = None
-    if flush is not None:   # cfg1 also hot (back to back, no flush)
-        a.record(st)
+    if flush is not None:   # cfg1 also hot (no flush; per-step events like the flushed loop)
         for k in range(K):
+            sa[k].record(st)
             mux.mux_run_layer(part, i, wl.pool, step_sides[k][0], step_sides[k][1], times[k])
-        b.record(st)
+            sb[k].record(st)
         torch.cuda.synchronize()
-        hot = step_tokens(D) / (a.elapsed_time(b) / K * 1e-3)
+        hot = step_tokens(D) / (float(np.mean([sa[k].elapsed_time(sb[k]) for k in range(K)])) * 1e-3)
     if world > 1:
         tm = torch.tensor([t_step], device="cuda", dtype=torch.float64)
         dist.all_reduce(tm, op=dist.ReduceOp.MAX)

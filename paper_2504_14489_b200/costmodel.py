@@ -12,13 +12,16 @@ Coefficients are fitted by non-negative least squares (all terms are costs), one
 (side, SM count).  The paper reports max deviations of 8.16% (prefill) and 8.84% (decode)
 for its own kernels; `fit` returns ours.
 
-Host-side scheduling logic (no GPU work): evaluated by the C engine through
-`mux_cost_predict` with the same coefficients; this module fits and checks them.
+Host-side scheduling logic (no GPU work).  The C engine (csrc/engine.cu) evaluates the
+paper-form Eq.1 / Eq.2 coefficients passed in mux_engine_desc (dec_theta / pf_theta) for its
+best-fit split and N_PL; this module fits them, and also the wave-aware B200 variants below,
+which is where the accuracy claim of P:607 is checked (tests/test_costmodel.py).
 """
 from __future__ import annotations
 
 import dataclasses
 import json
+import math
 from typing import Dict, List, Sequence, Tuple
 
 import numpy as np
@@ -33,6 +36,76 @@ def prefill_features(r: Sequence[int], n: Sequence[int]) -> np.ndarray:
 def decode_features(r: Sequence[int]) -> np.ndarray:
     r = np.asarray(r, dtype=np.float64)
     return np.array([np.sum(r), float(len(r)), 1.0])
+
+
+# ---------------------------------------------------------------------------------------------
+# Wave-aware B200 variants (Eq.1w / Eq.2w).  Eq.1 / Eq.2's constant + linear terms cannot express
+# wave quantisation: a grid of CTAs runs in waves over the partition's SMs, so a layer's time is
+# the MAKESPAN of its CTAs on k SMs, not the sum of their work / k (r01: Eq.1 missed by up to 35 %
+# on 132-148 SMs).  The features below keep the paper's physics (per-CTA work ~ the keys a q tile
+# attends, Table 2 P:588-590; decode work ~ reused context) but schedule it the way these kernels
+# launch: one CTA per SM, CTAs dispatched in launch order onto the first free SM.
+
+def _list_makespan(durations, k: int) -> float:
+    import heapq
+    h = [0.0] * max(1, min(k, len(durations)))
+    heapq.heapify(h)
+    span = 0.0
+    for t in durations:
+        s = heapq.heappop(h)
+        heapq.heappush(h, s + t)
+        span = max(span, s + t)
+    return span
+
+
+def prefill_wave_features(r: Sequence[int], n: Sequence[int], sms: int, hq: int = 32, hkv: int = 8, d: int = 128,
+                          cta_overhead_tiles: float = 1.0) -> np.ndarray:
+    """[attention makespan (128-key tile units), out-projection waves, sum n, 1] of one layer on
+    `sms` SMs: the prefill grid (q tile x head pair x sequence, csrc/prefill.cu tile_coord order:
+    q tiles longest-first grid-wide when the batch K/V is <= 64 MB, else per sequence heavy-first)
+    and the CTA-pair out-projection GEMM (256 x 256 tiles of T x hidden over sms/2 pairs)."""
+    keys = sum(a + b for a, b in zip(r, n))
+    nq = max((x + 127) // 128 for x in n)
+    heads = max(1, hq // 2)
+    ctas = []
+    def cta(b, qi):
+        return cta_overhead_tiles + math.ceil((r[b] + min((qi + 1) * 128, n[b])) / 128)
+    if keys * hkv * 4 * d <= 64 * 2 ** 20:
+        for qi in range(nq - 1, -1, -1):
+            for b in range(len(n)):
+                if qi * 128 < n[b]:
+                    ctas += [cta(b, qi)] * heads
+    else:
+        for b in sorted(range(len(n)), key=lambda i: -n[i] * (r[i] + 0.5 * n[i])):
+            for _ in range(heads):
+                ctas += [cta(b, qi) for qi in range((n[b] + 127) // 128 - 1, -1, -1)]
+    T = sum(n)
+    waves = math.ceil(math.ceil(T / 256) * 16 / max(1, sms // 2))
+    return np.array([_list_makespan(ctas, sms), float(waves), float(T), 1.0])
+
+
+def decode_wave_features(r: Sequence[int], sms: int, hkv: int = 8, d: int = 128, num_splits: int = 0,
+                         cta_overhead_pages: float = 10.0) -> np.ndarray:
+    """[CTA makespan (page units), sum r, bs, bs x splits (combine, split > 1), split > 1, 1] of one
+    decode layer on `sms` SMs: balanced split-KV CTAs (every split of a sequence covers
+    ceil(max_pages / S) pages, csrc/decode.cu) in launch order; S from the library's own
+    split heuristic (mux_decode_num_splits) unless given."""
+    L = [int(x) + 1 for x in r]
+    B = len(L)
+    if num_splits <= 0:
+        from . import binding
+        num_splits = binding.mux_decode_num_splits(B, hkv, max(L), sms, L, d)
+    S = num_splits
+    maxp = max((x + 15) // 16 for x in L)
+    C = math.ceil(maxp / S)
+    durs = []
+    for x in L:
+        p = (x + 15) // 16
+        for sp in range(S):
+            npg = max(0, min(C, p - sp * C)) if sp < S - 1 else max(0, p - sp * C)
+            durs.append(cta_overhead_pages + npg if (npg > 0 or sp == 0) else 2.0)
+    split = 1.0 if S > 1 else 0.0
+    return np.array([_list_makespan(durs, sms), float(sum(r)), float(B), B * S * split, split, 1.0])
 
 
 @dataclasses.dataclass

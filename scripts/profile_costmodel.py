@@ -135,6 +135,17 @@ def main():
         return out
     model = cm.CostModel(fits("prefill"), fits("decode"))
 
+    def wave_fits(kind):   # Eq.1w / Eq.2w (costmodel.prefill_wave_features / decode_wave_features)
+        out = {}
+        for sms in sorted({s["sms"] for s in samples[kind]}):
+            rows = [s for s in samples[kind] if s["sms"] == sms]
+            X = np.stack([cm.prefill_wave_features(s["r"], s["n"], sms) if kind == "prefill"
+                          else cm.decode_wave_features(s["r"], sms) for s in rows])
+            f = cm.fit(X, np.array([s["us_per_layer"] for s in rows]))
+            out[str(sms)] = {"theta": f.theta.tolist(), "max_dev": f.max_dev, "mean_dev": f.mean_dev, "n": f.n}
+        return out
+    wave = {"prefill_eq1w": wave_fits("prefill"), "decode_eq2w": wave_fits("decode")}
+
     # contention guard: co-run pairs on each split; side windows balanced with the solo model
     pairs_pf = [([0], [2048]), ([0], [8192]), ([8192] * 4, [1024] * 4)]
     pairs_dc = [[4095] * 64, [8191] * 128, [1023] * 32]
@@ -161,7 +172,7 @@ def main():
     for g in guard:
         model.max_slowdown_dec[g["dec_sms"]] = max(model.max_slowdown_dec.get(g["dec_sms"], 1.0), g["slowdown_dec"])
         model.max_slowdown_pf[g["pf_sms"]] = max(model.max_slowdown_pf.get(g["pf_sms"], 1.0), g["slowdown_pf"])
-    out = {"model": model.to_json(), "samples": samples, "guard": guard,
+    out = {"model": model.to_json(), "wave_aware": wave, "samples": samples, "guard": guard,
            "shapes": {"Hq": Hq, "Hkv": Hkv, "d": D, "hidden": HIDDEN}}
     with open(args.out, "w") as f:
         json.dump(out, f, indent=1)
@@ -169,6 +180,9 @@ def main():
         for sms, ft in sorted(d.items()):
             print(f"{kind} {sms:3d} SMs: theta {np.array2string(ft.theta, precision=4)} "
                   f"max dev {100 * ft.max_dev:.1f}% mean {100 * ft.mean_dev:.1f}% (n={ft.n})")
+    for kind, d in wave.items():
+        for sms, ft in d.items():
+            print(f"{kind} {int(sms):3d} SMs: max dev {100 * ft['max_dev']:.1f}% mean {100 * ft['mean_dev']:.1f}%")
     print("max slowdown dec", model.max_slowdown_dec)
     print("max slowdown pf", model.max_slowdown_pf)
     part.close()

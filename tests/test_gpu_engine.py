@@ -283,11 +283,15 @@ def test_engine_graphs_cut_launch_gap(mux, part):
         tr = eng.trace()
         dec = tr[tr[:, 0] == 0]
         s["iter_us"] = float(np.median(dec[:, 4] - dec[:, 3])) * 1e-3
+        # median interval between consecutive iteration ends (the mean also carries the few
+        # iterations that first capture + instantiate a graph, ~1 ms each)
+        s["tbt_median_us"] = float(np.median(np.diff(np.sort(dec[:, 4])))) * 1e-3
         res[mode] = s
         eng.close()
     for m, s in res.items():
         print(f"{m}: gap mean {s['gap_mean_us']:.1f} us max {s['gap_max_us']:.1f}, iteration {s['iter_us']:.1f} us, "
-              f"tbt {s['tbt_mean_us']:.1f} us, graphs {s['graphs']} ({s['graph_bytes']} B)")
+              f"tbt mean {s['tbt_mean_us']:.1f} / median {s['tbt_median_us']:.1f} us, graphs {s['graphs']} "
+              f"({s['graph_bytes']} B)")
     assert res["graphs"]["graphs"] >= 1 and res["kernels"]["graphs"] == 0
     assert res["graphs+overlap"]["gap_mean_us"] < res["kernels"]["gap_mean_us"]
-    assert res["graphs+overlap"]["tbt_mean_us"] < res["kernels"]["tbt_mean_us"]
+    assert res["graphs+overlap"]["tbt_median_us"] < res["kernels"]["tbt_median_us"]
