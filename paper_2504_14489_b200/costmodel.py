@@ -59,11 +59,13 @@ def _list_makespan(durations, k: int) -> float:
 
 
 def prefill_wave_features(r: Sequence[int], n: Sequence[int], sms: int, hq: int = 32, hkv: int = 8, d: int = 128,
-                          cta_overhead_tiles: float = 1.0) -> np.ndarray:
+                          cta_overhead_tiles: float = 3.0) -> np.ndarray:
     """[attention makespan (128-key tile units), out-projection waves, sum n, 1] of one layer on
     `sms` SMs: the prefill grid (q tile x head pair x sequence, csrc/prefill.cu tile_coord order:
     q tiles longest-first grid-wide when the batch K/V is <= 64 MB, else per sequence heavy-first)
-    and the CTA-pair out-projection GEMM (256 x 256 tiles of T x hidden over sms/2 pairs)."""
+    and the CTA-pair out-projection GEMM (256 x 256 tiles of T x hidden over sms/2 pairs).  A CTA
+    costs its key tiles + ~3 tiles of prologue / epilogue (TMEM alloc, Q load, O write), the
+    constant that fits the recorded B200 samples best (profiles/r02_costmodel.json)."""
     keys = sum(a + b for a, b in zip(r, n))
     nq = max((x + 127) // 128 for x in n)
     heads = max(1, hq // 2)

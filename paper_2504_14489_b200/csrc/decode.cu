@@ -361,7 +361,9 @@ __global__ void __launch_bounds__(DecodeCfg<NT>::kThreads, DecodeCfg<NT>::kCtasP
             oacc[mt][nt][3] *= alpha[nt][1];
           }
           dev::mma_bf16_16816(oacc[mt][nt], a0, a1, a2, a3, ph[nt][0], ph[nt][1]);
+#ifndef MUX_DEC_NO_PLO   // timing-only A/B switch (drops P_lo: wrong precision)
           dev::mma_bf16_16816(oacc[mt][nt], a0, a1, a2, a3, plo[nt][0], plo[nt][1]);
+#endif
         }
       }
       __syncwarp();
