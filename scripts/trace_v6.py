@@ -29,9 +29,10 @@ print("j  " + " ".join(f"{n:>7s}" for n in ev))
 for j in list(range(0, 4)) + list(range(30, 34)) + list(range(nt - 3, nt)):
     print(f"{j:2d} " + " ".join(f"{(t[e, j] - t0) if t[e, j] else -1:7d}" for e in ev.values()))
 mid = slice(8, nt - 4)
-for h, (qk, s, mx, ex, pv) in enumerate([(8, 0, 2, 12, 6), (9, 1, 3, 13, 7)]):
+for h, (qk, s, mx, ex, pv, pw) in enumerate([(8, 0, 2, 12, 6, 4), (9, 1, 3, 13, 7, 5)]):
     print(f"head {h}: period(S ready) {np.median(np.diff(t[s, :nt])[mid]):.0f}  qk->S {np.median((t[s]-t[qk])[mid]):.0f}"
           f"  S->max {np.median((t[mx]-t[s])[mid]):.0f}  max->P written {np.median((t[ex]-t[mx])[mid]):.0f}"
+          f"  (max->PV(j-1) seen done {np.median((t[pw]-t[mx])[mid]):.0f})"
           f"  P->PV issue {np.median((t[pv]-t[ex])[mid]):.0f}")
 print("B's S after A's S:", np.median((t[1] - t[0])[mid]), " A's QK(j+1) after B's S(j):",
       np.median((t[8, 1:nt] - t[1, :nt - 1])[mid]))
