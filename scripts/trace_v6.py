@@ -43,3 +43,13 @@ if (kl > 0).all() and (vl > 0).all():
       np.median((kl[2:] - t[9, :nt - 2])[mid]))
   print("V(j) issued -> PV_A(j) issued", np.median((t[6, :nt] - vl)[mid]), " V(j) issued after PV_B(j-3) issued",
       np.median((vl[3:] - t[7, :nt - 3])[mid]))
+
+# MMA issuer waits (v6 trace slots 10/11: QK_A(j+1) S free / K(j+1) landed; 14/15: PV_B(j-1) P ready / V ready)
+if (t[10, 8:nt - 4] > 0).all():
+    print("iteration j: MMA thread times relative to S_B(j) ready:")
+    print("  PV_B(j-1) P_B ready", np.median((t[14, :nt] - t[1, :nt])[mid]),
+          " V(j-1) ready", np.median((t[15, :nt] - t[1, :nt])[mid]),
+          " PV_B(j-1) issued", np.median((t[7, :nt - 1] - t[1, 1:nt])[mid]))
+    print("  QK_A(j+1) S free", np.median((t[10, :nt] - t[1, :nt])[mid]),
+          " K(j+1) landed", np.median((t[11, :nt] - t[1, :nt])[mid]),
+          " QK_A(j+1) issued", np.median((t[8, 1:nt] - t[1, :nt - 1])[mid]))

@@ -8,6 +8,7 @@ __device__ __forceinline__ uint64_t ffma2(uint64_t a, uint64_t b, uint64_t c) { 
 __device__ __forceinline__ uint64_t fadd2(uint64_t a, uint64_t b) { uint64_t d; asm("add.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b)); return d; }
 __device__ __forceinline__ float ex2(float x) { float y; asm volatile("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x)); return y; }
 __device__ __forceinline__ uint32_t pack_bf16(float lo, float hi) { uint32_t r; asm("cvt.rn.bf16x2.f32 %0, %1, %2;" : "=r"(r) : "f"(hi), "f"(lo)); return r; }
+__device__ __forceinline__ uint32_t pack_f16(float lo, float hi) { uint32_t r; asm("cvt.rn.f16x2.f32 %0, %1, %2;" : "=r"(r) : "f"(hi), "f"(lo)); return r; }
 template <int MODE>
 __global__ void k(const float* in, uint32_t* out, long long* cyc, int rows, float sl2, float m) {
   float s[128];
@@ -26,7 +27,9 @@ __global__ void k(const float* in, uint32_t* out, long long* cyc, int rows, floa
       else { e0 = ex2(a); e1 = ex2(b); }
       const uint64_t e = f2pack(e0, e1);
       acc = fadd2(acc, e);
-      if (MODE != 2) {                      // MODE 2: exp + sum only
+      if (MODE == 3) sink ^= pack_f16(e0, e1);        // the prefill v6 mix: FFMA2, 2 ex2, FADD2, F2FP.F16
+      if (MODE == 4) sink ^= pack_bf16(e0, e1);       // same with a bf16 pack
+      if (MODE < 2) {                      // MODE 2: exp + sum only
         const uint32_t u0 = __float_as_uint(e0) & 0xFFFF0000u, u1 = __float_as_uint(e1) & 0xFFFF0000u;
         uint32_t hi = __byte_perm(__float_as_uint(e0), __float_as_uint(e1), 0x7632);
         float r0, r1;
@@ -46,13 +49,15 @@ int main() {
   float* in; uint32_t* out; long long* cyc;
   cudaMalloc(&in, 4096 * 4); cudaMemset(in, 0, 4096 * 4);
   cudaMalloc(&out, 148 * 1024 * 4); cudaMalloc(&cyc, 148 * 8);
-  const char* mn[] = {"full (exp+sum+hi/lo)", "no MUFU", "exp+sum only"};
-  for (int mode = 0; mode < 3; ++mode)
-    for (int warps : {4, 8}) {
+  const char* mn[] = {"full (exp+sum+hi/lo)", "no MUFU", "exp+sum only", "v6 mix (f16 pack)", "v6 mix (bf16 pack)"};
+  for (int mode = 0; mode < 5; ++mode)
+    for (int warps : {4, 8, 16}) {
       auto run = [&] {
         if (mode == 0) k<0><<<148, warps * 32>>>(in, out, cyc, 200, 0.1f, 1.f);
         if (mode == 1) k<1><<<148, warps * 32>>>(in, out, cyc, 200, 0.1f, 1.f);
         if (mode == 2) k<2><<<148, warps * 32>>>(in, out, cyc, 200, 0.1f, 1.f);
+        if (mode == 3) k<3><<<148, warps * 32>>>(in, out, cyc, 200, 0.1f, 1.f);
+        if (mode == 4) k<4><<<148, warps * 32>>>(in, out, cyc, 200, 0.1f, 1.f);
       };
       run(); cudaDeviceSynchronize(); run(); cudaDeviceSynchronize();
       long long c; cudaMemcpy(&c, cyc, 8, cudaMemcpyDeviceToHost);
