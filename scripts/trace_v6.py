@@ -16,11 +16,11 @@ b = mux.Batch([0, N], [N], pi, pd)
 q = torch.randn((N, Hq, d), device="cuda").to(torch.bfloat16)
 o = torch.empty((N, Hq, d), device="cuda", dtype=torch.bfloat16)
 mux.mux_prefill_attn(pool, 0, b, Hq, q, o)
-tr = torch.zeros(16 * 256, dtype=torch.int64, device="cuda")
+tr = torch.zeros(24 * 256, dtype=torch.int64, device="cuda")
 os.environ["MUX_PF_TRACE"] = str(tr.data_ptr())
 mux.mux_prefill_attn(pool, 0, b, Hq, q, o)
 torch.cuda.synchronize()
-t = tr.view(16, 256).cpu().numpy().astype(np.int64)
+t = tr.view(24, 256).cpu().numpy().astype(np.int64)
 np.save("gpurun_out/trace_v6.npy", t)
 nt = 64
 t0 = t[t > 0].min()
@@ -53,3 +53,10 @@ if (t[10, 8:nt - 4] > 0).all():
     print("  QK_A(j+1) S free", np.median((t[10, :nt] - t[1, :nt])[mid]),
           " K(j+1) landed", np.median((t[11, :nt] - t[1, :nt])[mid]),
           " QK_A(j+1) issued", np.median((t[8, 1:nt] - t[1, :nt - 1])[mid]))
+
+# producer (slots 16/17: K(j) / V(j) loads issued once their ring slot was free), relative to S_B(j)
+if (t[16, 8:nt - 4] > 0).all():
+    print("producer relative to S_B(j): K(j+1) issued", np.median((t[16, 1:nt] - t[1, :nt - 1])[mid]),
+          " V(j) issued", np.median((t[17, :nt] - t[1, :nt])[mid]),
+          " V(j+1) issued", np.median((t[17, 1:nt] - t[1, :nt - 1])[mid]))
+    print("  K(j+1) issued -> landed (MMA saw it)", np.median((t[11, :nt - 1] - t[16, 1:nt])[mid]))
