@@ -162,7 +162,7 @@ class Workload:
         shape = (self.layers, pages, self.Hkv, 16, self.d)
         # the cached prefix / decode context of every layer: resident synthetic KV (N(0,1) bf16)
         self.kpool = torch.empty(shape, dtype=torch.bfloat16, device=dev)
-        self.vpool = torch.empty(shape, dtype=torch.bfloat16, device=dev)
+        self.vpool = torch.empty(shape, dtype=torch.float16, device=dev)   # the V cache is fp16 (R25)
         for l in range(self.layers):
             self.kpool[l].normal_(generator=g)
             self.vpool[l].normal_(generator=g)

@@ -81,7 +81,9 @@ typedef struct {
   int32_t num_kv_heads;  /* Hkv held by THIS pool (the local shard under KV-head sharding) */
   int32_t head_dim;      /* 64 or 128 */
   void* k_storage;       /* device, 16-B aligned, num_layers*num_pages*Hkv*16*d bf16; NULL => library cudaMalloc */
-  void* v_storage;       /* device, same shape; must be both NULL or both non-NULL */
+  void* v_storage;       /* device, same shape, IEEE fp16 (binary16): mux_append_kv stores V rows as fp16
+                            (R25, exact for bf16 values in [2^-14, 65504]); K stays bf16;
+                            must be both NULL or both non-NULL */
   uint64_t free_list_seed;
 } mux_pool_desc;
 
@@ -99,9 +101,9 @@ int mux_pool_refcount(mux_pool_t pool, int32_t page, int32_t* out);
 int mux_pool_free_list(mux_pool_t pool, int32_t* out, int32_t cap, int32_t* n_out);
 int mux_pool_storage(mux_pool_t pool, void** k_storage, void** v_storage);
 /* Sticky device-side error bits of kernels that used this pool (synchronises the device).
- * bit 0 (MUX_POOL_ERR_V_RANGE): the prefill kernel met a V value with |v| >= 65536, outside the
- * fp16 range its P.V product runs in; the value was clamped to
- * +-65504 and that call's output is not within tolerance.  clear != 0 resets the bits. */
+ * bit 0 (MUX_POOL_ERR_V_RANGE): mux_append_kv met a V value with |v| >= 65536, outside the fp16
+ * range the V cache is stored in (R25, "P precision"); the value was clamped to
+ * +-65504 and attention over it is not within tolerance.  clear != 0 resets the bits. */
 #define MUX_POOL_ERR_V_RANGE 1u
 int mux_pool_error_flags(mux_pool_t pool, uint32_t* flags, int32_t clear);
 
@@ -132,7 +134,9 @@ typedef struct {
   const int32_t* h_page_ids;
 } mux_batch;
 
-/* a2: write the new tokens' K/V rows into their pool slots of `layer` (bit-exact copy).
+/* a2: write the new tokens' K/V rows into their pool slots of `layer`: K as a bit-exact copy, V
+ * converted to the pool's fp16 (R25; exact for bf16 values in [2^-14, 65504], larger magnitudes
+ * clamp to +-65504 and set MUX_POOL_ERR_V_RANGE).
  * k_new, v_new: device bf16 [total_q][Hkv][d]; row qo_indptr[b]+i -> position L_b-n_b+i. */
 int mux_append_kv(mux_pool_t pool, int32_t layer, const mux_batch* batch,
                   const void* k_new, const void* v_new, mux_stream_t stream);
@@ -282,6 +286,33 @@ int mux_outproj(const void* x, const void* w_packed, void* y, int32_t y_dtype, i
  * device): also the TC(k_p) dense-GEMM denominator of SURVEY §8(d) on a green context */
 int mux_outproj_sms(const void* x, const void* w_packed, void* y, int32_t y_dtype, int32_t T, int32_t K,
                     int32_t N, mux_stream_t stream, int32_t num_sms);
+
+/* ------------------------------------------------------------------------------------
+ * f4 (first part): QKV projection + RoPE + KV append, ONE kernel.
+ * PAPER: each transformer layer = attention + FFN; the attention layer's projections
+ * are Table 2's n d^2 terms; "attention ... generates the keys and values of new
+ * tokens ... stored in a KV cache".  Llama-3 models (P:245 cites Llama 3; the
+ * evaluation serves Llama-3-8B / 70B) rotate q and k with RoPE (R26).
+ *
+ * Y = X . W_qkv, X [total_q][hidden] bf16 row-major (row = new token, in batch order),
+ * W_qkv = [hidden][(Hq + 2 Hkv) * 128] bf16 PACKED by mux_outproj_pack_w, columns = Hq query
+ * heads, then Hkv key heads, then Hkv value heads (128 each), fp32 accumulation (tcgen05, CTA
+ * pairs).  For the token at position p = L_b - n_b + i of sequence b (as mux_append_kv):
+ *   query heads: RoPE(p), stored bf16 to q_out [total_q][Hq][128];
+ *   key heads:   RoPE(p), stored bf16 into the token's slot of `layer` in the pool;
+ *   value heads: stored fp16 (R25) into the slot (|v| > 65504 clamps, MUX_POOL_ERR_V_RANGE).
+ * RoPE (R26, rotate-half): (y_c, y_{c+64}) -> (y_c cos a - y_{c+64} sin a, y_{c+64} cos a + y_c sin a),
+ * a = p * theta^(-2c/128), c < 64, with (cos a, sin a) read from `rope`, a device table
+ * [rope_max_pos][64] float2 made by mux_rope_table (double precision, rounded to fp32 once).
+ * Requirements: head_dim 128, Hq and Hkv even, Hq % Hkv == 0, hidden % 8 == 0, 16-byte aligned
+ * pointers, every position < rope_max_pos (checked on the host when the batch has host copies;
+ * on the device a position past the table skips the rotation and sets error bit 2).
+ * Replaces mux_append_kv for the batch's rows (same page-sharing checks). */
+size_t mux_rope_table_bytes(int32_t max_pos, int32_t head_dim);
+int mux_rope_table(void* table, int32_t max_pos, int32_t head_dim, double theta, mux_stream_t stream);
+int mux_qkv_rope_append(mux_pool_t pool, int32_t layer, const mux_batch* batch, int32_t num_q_heads,
+                        const void* x, int32_t hidden, const void* w_qkv_packed, const void* rope,
+                        int32_t rope_max_pos, void* q_out, mux_stream_t stream);
 
 /* bytes of the packed layout of a [K][N] weight: ceil(N/128) * ceil(K/64) * 16384 */
 size_t mux_outproj_packed_bytes(int32_t K, int32_t N);

@@ -63,7 +63,8 @@ def num_threads() -> int:
 
 
 def append(kpool: np.ndarray, vpool: np.ndarray, k_new, v_new, new_indptr, kv_len, page_indptr, page_ids):
-    """O2.  kpool/vpool: uint16 [num_pages, Hkv, 16, d] (ONE layer), modified in place."""
+    """O2.  kpool/vpool: uint16 [num_pages, Hkv, 16, d] (ONE layer), modified in place.  K rows are
+    copied (bf16 bits); V rows are stored as fp16 bits (R25)."""
     assert kpool.dtype == np.uint16 and kpool.flags.c_contiguous and vpool.flags.c_contiguous
     num_pages, Hkv, P, d = kpool.shape
     assert P == 16
@@ -78,7 +79,7 @@ def append(kpool: np.ndarray, vpool: np.ndarray, k_new, v_new, new_indptr, kv_le
 
 def attention(q, kpool, vpool, qo_indptr, kv_len, page_indptr, page_ids, scale: Optional[float] = None,
               rows: Optional[np.ndarray] = None):
-    """O3/O4.  q: uint16 [total_q, Hq, d]; pools: uint16 [num_pages, Hkv, 16, d].
+    """O3/O4.  q: uint16 [total_q, Hq, d]; pools: uint16 [num_pages, Hkv, 16, d] (K bf16, V fp16 bits).
     Returns (out float64 [n_rows, Hq, d], lse float64 [n_rows, Hq])."""
     q = _c(q, np.uint16)
     total_q, Hq, d = q.shape
@@ -133,6 +134,10 @@ def outproj(o_rows: np.ndarray, w_o_bits: np.ndarray) -> np.ndarray:
     if o_rows.dtype == np.uint16:
         o_rows = bf16_to_double(o_rows)
     return np.matmul(o_rows.astype(np.float64), bf16_to_double(w_o_bits))
+
+
+def f16_to_double(bits: np.ndarray) -> np.ndarray:
+    return np.ascontiguousarray(bits, dtype=np.uint16).view(np.float16).astype(np.float64)
 
 
 def bf16_to_double(bits: np.ndarray) -> np.ndarray:

@@ -18,9 +18,10 @@
 //     online softmax per head column with a lazy reference max (moves only when a score exceeds it
 //     by > 8); the exact page max (warp shuffles over the 8 token lanes) only when a warp vote
 //     says some column grew
-//     P^T -> B fragments with movmatrix.trans (no smem round trip), P = P_hi + P_lo in
-//     two bf16 halves (~16-bit P)
-//     O^T[d x 8] += V_page^T . P_hi^T + V_page^T . P_lo^T (A = V^T via ldmatrix.trans)
+//     P^T -> B fragments with movmatrix.trans (no smem round trip), P in fp16 (11-bit, DESIGN.md
+//     "P precision"), which the fp16 V cache (R25) allows in ONE mma per tile (r01: bf16 V needed
+//     P = P_hi + P_lo, two bf16 MMAs)
+//     O^T[d x 8] += V_page^T . P^T (A = V^T via ldmatrix.trans, fp16)
 //   Warps merge their (m, l, O) states in smem at the end; with one split the CTA writes
 //   the normalised output, otherwise fp32 partials (o, m, l) for the combine kernel.
 //   Per SM the kernel is bound by the shared-memory port (TMA writes + ldmatrix reads of every KV
@@ -278,7 +279,7 @@ __global__ void __launch_bounds__(DecodeCfg<NT>::kThreads, DecodeCfg<NT>::kCtasP
       }
       // ---- online softmax (log2 domain); thread holds tokens g4, g4+8 x heads 2q, 2q+1
       const bool v0 = g4 < valid, v1 = (g4 + 8) < valid;
-      uint32_t ph[NT][2], plo[NT][2];
+      uint32_t ph[NT][2];
       float alpha[NT][2];
       float x[NT][4];
       bool grow = false;   // does any score exceed its column's reference max by more than 8?
@@ -291,7 +292,7 @@ __global__ void __launch_bounds__(DecodeCfg<NT>::kThreads, DecodeCfg<NT>::kCtasP
         grow |= (fmaxf(x[nt][0], x[nt][2]) > m_run[nt][0] + 8.f) | (fmaxf(x[nt][1], x[nt][3]) > m_run[nt][1] + 8.f);
       }
       // lazy rescale (FA4-style): a column's reference max moves only when the page max exceeds it by
-      // more than 8 (P <= 2^8 stays exact enough in P_hi + P_lo); otherwise alpha = 1 and the O
+      // more than 8 (P <= 2^8 stays far inside fp16's range); otherwise alpha = 1 and the O
       // rescale below is skipped.  The exact page max (3 shuffle rounds per column on the page's
       // critical path) is only needed when some column grows, which one warp vote tells (after the
       // first page: rarely); the result is the same as always taking the max.
@@ -317,14 +318,9 @@ __global__ void __launch_bounds__(DecodeCfg<NT>::kThreads, DecodeCfg<NT>::kCtasP
         const float p2 = dev::ex2(x[nt][2] - mn0), p3 = dev::ex2(x[nt][3] - mn1);
         l_run[nt][0] = l_run[nt][0] * alpha[nt][0] + p0 + p2;
         l_run[nt][1] = l_run[nt][1] * alpha[nt][1] + p1 + p3;
-        // P = P_hi + P_lo, both bf16: ~16 significant bits
-        const uint32_t h01 = dev::pack_bf16(p0, p1), h23 = dev::pack_bf16(p2, p3);
-        const uint32_t l01 = dev::pack_bf16(p0 - dev::bf16lo(h01), p1 - dev::bf16hi(h01));
-        const uint32_t l23 = dev::pack_bf16(p2 - dev::bf16lo(h23), p3 - dev::bf16hi(h23));
-        ph[nt][0] = dev::movmatrix_t(h01);    // tokens 0-7  -> b0
-        ph[nt][1] = dev::movmatrix_t(h23);    // tokens 8-15 -> b1
-        plo[nt][0] = dev::movmatrix_t(l01);
-        plo[nt][1] = dev::movmatrix_t(l23);
+        // P in fp16: 11 significant bits, against the fp16 V cache
+        ph[nt][0] = dev::movmatrix_t(dev::pack_f16(p0, p1));    // tokens 0-7  -> b0
+        ph[nt][1] = dev::movmatrix_t(dev::pack_f16(p2, p3));    // tokens 8-15 -> b1
       }
       dev::mbar_wait(&vfull[s], (i / STAGES) & 1);
       if (valid < kPage) {
@@ -337,7 +333,7 @@ __global__ void __launch_bounds__(DecodeCfg<NT>::kThreads, DecodeCfg<NT>::kCtasP
           }
         __syncwarp();
       }
-      // ---- O^T[half] = alpha * O^T[half] + V^T[half] . (P_hi + P_lo)^T
+      // ---- O^T[half] = alpha * O^T[half] + V^T[half] . P^T  (fp16 x fp16, fp32 accumulate)
       bool rescale = false;   // alpha != 1 only where a column grew (so never without `grow`)
       if (grow) {
 #pragma unroll
@@ -360,10 +356,7 @@ __global__ void __launch_bounds__(DecodeCfg<NT>::kThreads, DecodeCfg<NT>::kCtasP
             oacc[mt][nt][2] *= alpha[nt][0];
             oacc[mt][nt][3] *= alpha[nt][1];
           }
-          dev::mma_bf16_16816(oacc[mt][nt], a0, a1, a2, a3, ph[nt][0], ph[nt][1]);
-#ifndef MUX_DEC_NO_PLO   // timing-only A/B switch (drops P_lo: wrong precision)
-          dev::mma_bf16_16816(oacc[mt][nt], a0, a1, a2, a3, plo[nt][0], plo[nt][1]);
-#endif
+          dev::mma_f16_16816(oacc[mt][nt], a0, a1, a2, a3, ph[nt][0], ph[nt][1]);
         }
       }
       __syncwarp();

@@ -204,6 +204,45 @@ __global__ void __launch_bounds__(kGThreads, 1)
 // both CTAs' loads complete on the leader's full barrier; the leader's commits multicast to
 // both CTAs' empty / accumulator barriers; the peer's epilogue releases an accumulator with a
 // remote arrive on the leader's barrier.
+// f4 (QKV projection + RoPE + append, fused): the pair kernel's epilogue, per output row (token)
+// and 128-column head of Y = X . W_qkv: q heads get RoPE and go to q_out (bf16); k heads get RoPE
+// and go to the token's pool slot (bf16); v heads go to the pool slot as fp16 (R25).
+struct QkvParams {
+  const int32_t* qo_indptr;
+  const int32_t* kv_len;
+  const int32_t* page_indptr;
+  const int32_t* page_ids;
+  int num_seqs;
+  uint16_t* kpool;          // this layer's K pages [num_pages][Hkv][16][128]
+  uint16_t* vpool;
+  uint16_t* q_out;          // [T][Hq][128]
+  const float2* rope;       // [max_pos][64] (cos, sin), mux_rope_table
+  int rope_max_pos;
+  int hq, hkv;
+  int* err;                 // pool error word (V range, position past the table)
+};
+
+constexpr int kHeadD = 128;
+
+// y (128 fp32 of one head, one row) -> bf16 row at dst (16-byte stores)
+__device__ __forceinline__ void store_head_bf16(uint16_t* dst, const float* y) {
+#pragma unroll
+  for (int i = 0; i < kHeadD / 8; ++i)
+    reinterpret_cast<uint4*>(dst)[i] = make_uint4(dev::pack_bf16(y[8 * i], y[8 * i + 1]), dev::pack_bf16(y[8 * i + 2], y[8 * i + 3]),
+                                                  dev::pack_bf16(y[8 * i + 4], y[8 * i + 5]), dev::pack_bf16(y[8 * i + 6], y[8 * i + 7]));
+}
+
+// RoPE (R26, Llama rotate-half): (y_c, y_{c+64}) rotated by angle pos * theta^(-2c/128)
+__device__ __forceinline__ void rope_head(float* y, const float2* __restrict__ cs) {
+#pragma unroll
+  for (int c = 0; c < kHeadD / 2; ++c) {
+    const float2 t = __ldg(cs + c);
+    const float a = y[c], b = y[c + kHeadD / 2];
+    y[c] = a * t.x - b * t.y;
+    y[c + kHeadD / 2] = b * t.x + a * t.y;
+  }
+}
+
 constexpr int kP2Stages = 6;
 struct Gemm2Smem {
   static constexpr int kA = kGBM * kGBK * 2;          // 16 KiB: my 128 rows x 64 k
@@ -214,9 +253,10 @@ struct Gemm2Smem {
   static constexpr int kBytes = kTmemSlot + 16;
 };
 
+template <bool QKV>
 __global__ void __launch_bounds__(kGThreads, 1)
     outproj2_kernel(const __grid_constant__ CUtensorMap tmap_x, const __grid_constant__ CUtensorMap tmap_w,
-                    const GemmParams p) {
+                    const GemmParams p, const QkvParams qp) {
   using L = Gemm2Smem;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -294,6 +334,65 @@ __global__ void __launch_bounds__(kGThreads, 1)
       }
     }
     __syncwarp();
+  } else if (QKV) {
+    // fused QKV epilogue (both CTAs): my 128 rows (tokens) x 2 heads of TMEM buffer b
+    int i = 0;
+    for (int t = pair; t < tiles; t += npairs, ++i) {
+      const int b = i & 1;
+      const int m0 = (t / p.n_tiles) * 2 * kGBM + static_cast<int>(rank) * kGBM;
+      const int n0 = (t % p.n_tiles) * kGBN;
+      dev::mbar_wait_sleep(&acc_full[b], (i >> 1) & 1);
+      dev::tc_fence_after();
+      const int row = m0 + warp * 32 + lane;
+      // the token's sequence, position and pool slot (as mux_append_kv)
+      int pos = 0, page = 0;
+      if (row < p.T) {
+        int lo = 0, hi = qp.num_seqs - 1;
+        while (lo < hi) {
+          const int mid = (lo + hi + 1) >> 1;
+          if (__ldg(qp.qo_indptr + mid) <= row) lo = mid; else hi = mid - 1;
+        }
+        const int q0 = __ldg(qp.qo_indptr + lo), n = __ldg(qp.qo_indptr + lo + 1) - q0;
+        pos = __ldg(qp.kv_len + lo) - n + (row - q0);
+        page = __ldg(qp.page_ids + __ldg(qp.page_indptr + lo) + (pos >> 4));
+      }
+      const bool pos_ok = pos < qp.rope_max_pos;
+      if (row < p.T && !pos_ok && qp.err) atomicOr(qp.err, 2);
+      const uint32_t taddr = tmem + b * kGBN + (static_cast<uint32_t>(warp * 32) << 16);
+#pragma unroll 1
+      for (int hh = 0; hh < kGBN / kHeadD; ++hh) {
+        float y[kHeadD];
+#pragma unroll
+        for (int c = 0; c < kHeadD / 32; ++c) {
+          dev::tmem_ld32(taddr + hh * kHeadD + c * 32, *reinterpret_cast<uint32_t(*)[32]>(&y[32 * c]));
+        }
+        dev::tmem_wait_ld();
+        if (hh == kGBN / kHeadD - 1) {
+          dev::tc_fence_before();
+          __syncwarp();
+          if (lane == 0) dev::mbar_arrive_cluster(acc_empty_leader + b * 8);
+        }
+        const int gh = n0 / kHeadD + hh;             // global head column: q heads, k heads, v heads
+        if (row >= p.T || gh >= qp.hq + 2 * qp.hkv) continue;
+        if (gh < qp.hq + qp.hkv && pos_ok) rope_head(y, qp.rope + static_cast<size_t>(pos) * (kHeadD / 2));
+        if (gh < qp.hq) {
+          store_head_bf16(qp.q_out + (static_cast<size_t>(row) * qp.hq + gh) * kHeadD, y);
+        } else if (gh < qp.hq + qp.hkv) {
+          store_head_bf16(qp.kpool + ((static_cast<size_t>(page) * qp.hkv + (gh - qp.hq)) * kPage + (pos & 15)) * kHeadD, y);
+        } else {
+          uint16_t* dst = qp.vpool + ((static_cast<size_t>(page) * qp.hkv + (gh - qp.hq - qp.hkv)) * kPage + (pos & 15)) * kHeadD;
+          bool big = false;
+#pragma unroll
+          for (int c = 0; c < kHeadD; ++c) big |= fabsf(y[c]) > 65504.f;
+          if (big && qp.err) atomicOr(qp.err, MUX_POOL_ERR_V_RANGE);
+#pragma unroll
+          for (int k = 0; k < kHeadD / 8; ++k)
+            reinterpret_cast<uint4*>(dst)[k] =
+                make_uint4(dev::pack_f16_satfinite(y[8 * k], y[8 * k + 1]), dev::pack_f16_satfinite(y[8 * k + 2], y[8 * k + 3]),
+                           dev::pack_f16_satfinite(y[8 * k + 4], y[8 * k + 5]), dev::pack_f16_satfinite(y[8 * k + 6], y[8 * k + 7]));
+        }
+      }
+    }
   } else {
     // epilogue (both CTAs): my 128 rows x 256 columns of TMEM buffer b
     int i = 0;
@@ -539,7 +638,7 @@ int outproj_launch(const void* x, const void* w, void* y, int32_t y_dtype, int32
     static bool attr2 = false;
     const int smem2 = Gemm2Smem::kBytes + 1024;
     if (!attr2) {
-      MUX_CUDA(cudaFuncSetAttribute(outproj2_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem2));
+      MUX_CUDA(cudaFuncSetAttribute(outproj2_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem2));
       attr2 = true;
     }
     GemmParams prm{y, wp, T, N, K, y_dtype == MUX_DTYPE_F32, (T + 2 * kGBM - 1) / (2 * kGBM), (N + kGBN - 1) / kGBN};
@@ -558,7 +657,7 @@ int outproj_launch(const void* x, const void* w, void* y, int32_t y_dtype, int32
     attr[0].val.clusterDim.z = 1;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
-    const cudaError_t e = cudaLaunchKernelEx(&cfg, outproj2_kernel, tx, tw, prm);
+    const cudaError_t e = cudaLaunchKernelEx(&cfg, outproj2_kernel<false>, tx, tw, prm, QkvParams{});
     if (e == cudaSuccess) return MUX_OK;
     (void)cudaGetLastError();  // no CTA pairs on this partition: fall back to the single-CTA kernel
   }
@@ -576,6 +675,101 @@ int outproj_launch(const void* x, const void* w, void* y, int32_t y_dtype, int32
   return MUX_OK;
 }
 }  // namespace mux
+
+// ---------------------------------------------------------------- f4: RoPE table + fused QKV launch
+namespace mux {
+namespace {
+// (cos, sin) of pos * theta^(-2c/d) for c < d/2, computed in double and rounded to fp32 once
+__global__ void rope_table_kernel(float2* t, int max_pos, int half, double theta) {
+  const size_t n = static_cast<size_t>(max_pos) * half;
+  for (size_t i = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<size_t>(gridDim.x) * blockDim.x) {
+    const int pos = static_cast<int>(i / half), c = static_cast<int>(i % half);
+    const double a = pos * pow(theta, -2.0 * c / (2.0 * half));
+    double sn, cs;
+    sincos(a, &sn, &cs);
+    t[i] = make_float2(static_cast<float>(cs), static_cast<float>(sn));
+  }
+}
+}  // namespace
+}  // namespace mux
+
+extern "C" size_t mux_rope_table_bytes(int32_t max_pos, int32_t head_dim) {
+  if (max_pos < 1 || head_dim < 2) return 0;
+  return static_cast<size_t>(max_pos) * (head_dim / 2) * sizeof(float2);
+}
+
+extern "C" int mux_rope_table(void* table, int32_t max_pos, int32_t head_dim, double theta, mux_stream_t stream) {
+  if (!table || max_pos < 1 || head_dim != 128 || !(theta > 1.0))
+    return mux::fail(MUX_ERR_INVALID_ARG, "mux_rope_table: table, max_pos >= 1, head_dim 128, theta > 1 required");
+  const size_t n = static_cast<size_t>(max_pos) * (head_dim / 2);
+  const int blocks = static_cast<int>(std::min<size_t>((n + 255) / 256, 4096));
+  mux::rope_table_kernel<<<blocks, 256, 0, reinterpret_cast<cudaStream_t>(stream)>>>(static_cast<float2*>(table),
+                                                                                    max_pos, head_dim / 2, theta);
+  MUX_CUDA(cudaGetLastError());
+  return MUX_OK;
+}
+
+extern "C" int mux_qkv_rope_append(mux_pool_t pool, int32_t layer, const mux_batch* b, int32_t hq, const void* x,
+                                   int32_t hidden, const void* w_qkv, const void* rope, int32_t rope_max_pos,
+                                   void* q_out, mux_stream_t stream) {
+  using namespace mux;
+  int rc = check_pool_layer(pool, layer);
+  if (rc) return rc;
+  if ((rc = validate_batch(b, false))) return rc;
+  const int d = pool->desc.head_dim, hkv = pool->desc.num_kv_heads;
+  if (d != kHeadD) return fail(MUX_ERR_UNSUPPORTED, "mux_qkv_rope_append: head_dim must be 128");
+  if (hq < 2 || hq % hkv || (hq & 1) || (hkv & 1))
+    return fail(MUX_ERR_UNSUPPORTED, "mux_qkv_rope_append: Hq, Hkv even and Hq a multiple of Hkv");
+  if (!x || !w_qkv || !rope || !q_out) return fail(MUX_ERR_INVALID_ARG, "mux_qkv_rope_append: NULL pointer");
+  if (hidden < 8 || hidden % 8) return fail(MUX_ERR_UNSUPPORTED, "mux_qkv_rope_append: hidden must be a multiple of 8");
+  if ((reinterpret_cast<uintptr_t>(x) | reinterpret_cast<uintptr_t>(w_qkv) | reinterpret_cast<uintptr_t>(q_out)) & 15)
+    return fail(MUX_ERR_INVALID_ARG, "mux_qkv_rope_append: pointers must be 16-byte aligned");
+  if (b->h_kv_len)
+    for (int s2 = 0; s2 < b->num_seqs; ++s2)
+      if (b->h_kv_len[s2] > rope_max_pos) return fail(MUX_ERR_INVALID_ARG, "position past the RoPE table");
+  if ((rc = append_checks(pool, b))) return rc;
+  if ((rc = pool_tmaps(pool))) return rc;
+  const int T = b->total_q, K = hidden, N = (hq + 2 * hkv) * d;
+  CUtensorMap tx, tw;
+  uint64_t dx[3] = {static_cast<uint64_t>(K), static_cast<uint64_t>(T), 1};
+  uint64_t sx[2] = {static_cast<uint64_t>(K) * 2, static_cast<uint64_t>(K) * T * 2};
+  uint32_t bx[3] = {kGBK, kGBM, 1};
+  if ((rc = make_tmap_bf16(&tx, x, 3, dx, sx, bx))) return rc;
+  const int KB = (K + kGBK - 1) / kGBK, NT = (N + 127) / 128;
+  uint64_t dw[3] = {64, 128, static_cast<uint64_t>(KB) * NT};
+  uint64_t sw[2] = {128, 16384};
+  uint32_t bw[3] = {64, 128, 1};
+  if ((rc = make_tmap_bf16(&tw, w_qkv, 3, dw, sw, bw, false))) return rc;
+  static bool attr = false;
+  const int smem2 = Gemm2Smem::kBytes + 1024;
+  if (!attr) {
+    MUX_CUDA(cudaFuncSetAttribute(outproj2_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem2));
+    attr = true;
+  }
+  GemmParams prm{nullptr, static_cast<const uint8_t*>(w_qkv), T, N, K, 0, (T + 2 * kGBM - 1) / (2 * kGBM),
+                 (N + kGBN - 1) / kGBN};
+  const size_t off = static_cast<size_t>(layer) * pool->layer_elems();
+  QkvParams qp{b->qo_indptr, b->kv_len, b->page_indptr, b->page_ids, b->num_seqs,
+               static_cast<uint16_t*>(pool->desc.k_storage) + off, static_cast<uint16_t*>(pool->desc.v_storage) + off,
+               static_cast<uint16_t*>(q_out), static_cast<const float2*>(rope), rope_max_pos, hq, hkv, pool->d_err};
+  const int tiles = prm.m_tiles * prm.n_tiles;
+  const int pairs = std::max(1, std::min(tiles, device_sm_count() / 2));
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(2 * pairs);
+  cfg.blockDim = dim3(kGThreads);
+  cfg.dynamicSmemBytes = smem2;
+  cfg.stream = reinterpret_cast<cudaStream_t>(stream);
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeClusterDimension;
+  at[0].val.clusterDim.x = 2;
+  at[0].val.clusterDim.y = 1;
+  at[0].val.clusterDim.z = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  MUX_CUDA(cudaLaunchKernelEx(&cfg, outproj2_kernel<true>, tx, tw, prm, qp));
+  return MUX_OK;
+}
 
 extern "C" int mux_outproj(const void* x, const void* w, void* y, int32_t y_dtype, int32_t T, int32_t K, int32_t N,
                            mux_stream_t stream) {

@@ -53,6 +53,22 @@ int pool_tmaps(mux_pool* p) {
   return MUX_OK;
 }
 
+// host checks of a write of the batch's new rows (when the host copies of the tables are given):
+// page ids in range; no write into a page shared by another sequence (R13)
+int append_checks(mux_pool* p, const mux_batch* b) {
+  if (!(b->h_qo_indptr && b->h_kv_len && b->h_page_indptr && b->h_page_ids)) return MUX_OK;
+  for (int s = 0; s < b->num_seqs; ++s) {
+    int n = b->h_qo_indptr[s + 1] - b->h_qo_indptr[s];
+    int L = b->h_kv_len[s];
+    for (int pg = (L - n) / kPage; pg <= (L - 1) / kPage; ++pg) {
+      int id = b->h_page_ids[b->h_page_indptr[s] + pg];
+      if (id < 0 || id >= p->desc.num_pages) return fail(MUX_ERR_INVALID_ARG, "page id out of range");
+      if (p->ref[id] > 1) return fail(MUX_ERR_SHARED_PAGE_WRITE, "append would write a shared page");
+    }
+  }
+  return MUX_OK;
+}
+
 int check_pool_layer(mux_pool* p, int32_t layer) {
   if (!p) return fail(MUX_ERR_INVALID_ARG, "pool is NULL");
   if (layer < 0 || layer >= p->desc.num_layers) return fail(MUX_ERR_INVALID_ARG, "layer out of range");
@@ -69,7 +85,7 @@ __global__ void __launch_bounds__(256) append_kv_kernel(uint4* __restrict__ kpoo
                                                         const int32_t* __restrict__ kv_len,
                                                         const int32_t* __restrict__ page_indptr,
                                                         const int32_t* __restrict__ page_ids, int num_seqs,
-                                                        int chunks_per_head, int hkv) {
+                                                        int chunks_per_head, int hkv, int* __restrict__ err) {
   const int row = blockIdx.x;
   int lo = 0, hi = num_seqs - 1;  // last b with qo_indptr[b] <= row
   while (lo < hi) {
@@ -88,7 +104,16 @@ __global__ void __launch_bounds__(256) append_kv_kernel(uint4* __restrict__ kpoo
     const size_t dst = ((static_cast<size_t>(page) * hkv + h) * kPage + slot) * chunks_per_head + c;
     const size_t src = static_cast<size_t>(row) * row_chunks + i;
     kpool[dst] = __ldg(k_new + src);
-    vpool[dst] = __ldg(v_new + src);
+    // the V cache holds fp16 (R25): bf16 -> fp16 round-to-nearest-even, exact for every
+    // bf16 value in [2^-14, 65504]; larger magnitudes (bf16 >= 65536) clamp to +-65504 and flag the pool
+    uint4 w = __ldg(v_new + src);
+    const uint32_t mx = __vmaxu2(__vmaxu2(w.x & 0x7FFF7FFFu, w.y & 0x7FFF7FFFu), __vmaxu2(w.z & 0x7FFF7FFFu, w.w & 0x7FFF7FFFu));
+    if (__vmaxu2(mx, 0x477F477Fu) != 0x477F477Fu && err) atomicOr(err, MUX_POOL_ERR_V_RANGE);
+    w.x = dev::pack_f16_satfinite(dev::bf16lo(w.x), dev::bf16hi(w.x));
+    w.y = dev::pack_f16_satfinite(dev::bf16lo(w.y), dev::bf16hi(w.y));
+    w.z = dev::pack_f16_satfinite(dev::bf16lo(w.z), dev::bf16hi(w.z));
+    w.w = dev::pack_f16_satfinite(dev::bf16lo(w.w), dev::bf16hi(w.w));
+    vpool[dst] = w;
   }
 }
 
@@ -236,18 +261,8 @@ int mux_append_kv(mux_pool_t p, int32_t layer, const mux_batch* b, const void* k
   if (!k_new || !v_new) return fail(MUX_ERR_INVALID_ARG, "k_new/v_new NULL");
   if ((reinterpret_cast<uintptr_t>(k_new) | reinterpret_cast<uintptr_t>(v_new)) & 15)
     return fail(MUX_ERR_INVALID_ARG, "k_new/v_new must be 16-byte aligned");
-  if (b->h_qo_indptr && b->h_kv_len && b->h_page_indptr && b->h_page_ids) {
-    // host checks: ids in range; no write into a page shared by another sequence (R13)
-    for (int s = 0; s < b->num_seqs; ++s) {
-      int n = b->h_qo_indptr[s + 1] - b->h_qo_indptr[s];
-      int L = b->h_kv_len[s];
-      for (int pg = (L - n) / kPage; pg <= (L - 1) / kPage; ++pg) {
-        int id = b->h_page_ids[b->h_page_indptr[s] + pg];
-        if (id < 0 || id >= p->desc.num_pages) return fail(MUX_ERR_INVALID_ARG, "page id out of range");
-        if (p->ref[id] > 1) return fail(MUX_ERR_SHARED_PAGE_WRITE, "append would write a shared page");
-      }
-    }
-  }
+  if ((rc = append_checks(p, b))) return rc;
+  if ((rc = pool_tmaps(p))) return rc;   // also allocates the pool's device error word
   const int d = p->desc.head_dim, hkv = p->desc.num_kv_heads;
   const int chunks_per_head = d / 8;
   const size_t off = static_cast<size_t>(layer) * p->layer_elems();
@@ -256,7 +271,7 @@ int mux_append_kv(mux_pool_t p, int32_t layer, const mux_batch* b, const void* k
   int threads = std::min(256, std::max(32, ((chunks_per_head * hkv + 31) / 32) * 32));
   append_kv_kernel<<<b->total_q, threads, 0, reinterpret_cast<cudaStream_t>(stream)>>>(
       kp, vp, static_cast<const uint4*>(k_new), static_cast<const uint4*>(v_new), b->qo_indptr, b->kv_len,
-      b->page_indptr, b->page_ids, b->num_seqs, chunks_per_head, hkv);
+      b->page_indptr, b->page_ids, b->num_seqs, chunks_per_head, hkv, p->d_err);
   MUX_CUDA(cudaGetLastError());
   return MUX_OK;
 }

@@ -17,7 +17,7 @@ struct mux_pool {
   // tmap_kh: box = one 64-dim half of one (page, kv head) block (2 KiB)            -> prefill K
   CUtensorMap tmap_k1, tmap_v1, tmap_kg, tmap_vg, tmap_kh;
   int hg = 1;                        // kv heads per decode CTA (largest power of two <= 8 dividing Hkv)
-  int* d_err = nullptr;              // device error word (bit 0: prefill clamped a V value to fp16 range)
+  int* d_err = nullptr;              // device error word (bit 0: append clamped a V value to fp16 range)
   int64_t layer_elems() const {      // elements per layer of K (or V)
     return static_cast<int64_t>(desc.num_pages) * desc.num_kv_heads * mux::kPage * desc.head_dim;
   }
@@ -26,4 +26,5 @@ struct mux_pool {
 namespace mux {
 int pool_tmaps(mux_pool* p);  // build the K/V tensor maps on first use
 int check_pool_layer(mux_pool* p, int32_t layer);
+int append_checks(mux_pool* p, const mux_batch* b);  // host checks of a write of the new rows
 }  // namespace mux

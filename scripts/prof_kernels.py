@@ -10,7 +10,7 @@ import paper_2504_14489_b200 as mux  # noqa: E402
 Hq, Hkv, d, B, C, N = 32, 8, 128, 64, 4096, int(os.environ.get("NPF", 8192))
 num_pages = B * C // 16 + N // 16 + 16
 k = torch.randn((1, num_pages, Hkv, 16, d), device="cuda").to(torch.bfloat16)
-v = torch.randn((1, num_pages, Hkv, 16, d), device="cuda").to(torch.bfloat16)
+v = torch.randn((1, num_pages, Hkv, 16, d), device="cuda").to(torch.float16)
 pool = mux.Pool(1, num_pages, Hkv, d, 1, k, v)
 pi, pd = pool.page_tables([C // 16] * B)
 db = mux.Batch(list(range(B + 1)), [C] * B, pi, pd)

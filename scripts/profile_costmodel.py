@@ -53,7 +53,7 @@ class Bench:
     def __init__(self):
         max_pages = 128 * 8192 // 16 + 2 * 40960 // 16 + 64
         self.k = torch.empty((POOL_LAYERS, max_pages, Hkv, 16, D), dtype=torch.bfloat16, device="cuda").normal_()
-        self.v = torch.empty_like(self.k).normal_()
+        self.v = torch.empty_like(self.k, dtype=torch.float16).normal_()   # V cache: fp16 (R25)
         self.pool = mux.Pool(POOL_LAYERS, max_pages, Hkv, D, 11, self.k, self.v)
         self.w = mux.mux_outproj_pack_w((torch.randn((Hq * D, HIDDEN), device="cuda") / 64).to(torch.bfloat16))
         self.scale = 1 / math.sqrt(D)

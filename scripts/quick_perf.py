@@ -34,7 +34,7 @@ def main():
     pf_pages = (n_pf + 15) // 16
     num_pages = dc_pages + pf_pages + 16
     k = torch.randn((layers, num_pages, Hkv, 16, d), device="cuda").to(torch.bfloat16)
-    v = torch.randn((layers, num_pages, Hkv, 16, d), device="cuda").to(torch.bfloat16)
+    v = torch.randn((layers, num_pages, Hkv, 16, d), device="cuda").to(torch.float16)   # V cache: fp16 (R25)
     pool = mux.Pool(layers, num_pages, Hkv, d, 1, k, v)
     pind, pids = pool.page_tables([C // 16] * B)
     dbatch = mux.Batch(list(range(B + 1)), [C] * B, pind, pids)

@@ -9,7 +9,7 @@ import paper_2504_14489_b200 as mux  # noqa: E402
 Hq, Hkv, d, N = 32, 8, 128, 8192
 pages = N // 16 + 16
 k = torch.randn((1, pages, Hkv, 16, d), device="cuda").to(torch.bfloat16)
-v = torch.randn((1, pages, Hkv, 16, d), device="cuda").to(torch.bfloat16)
+v = torch.randn((1, pages, Hkv, 16, d), device="cuda").to(torch.float16)   # V cache: fp16 (R25)
 pool = mux.Pool(1, pages, Hkv, d, 1, k, v)
 pi, pd = pool.page_tables([N // 16])
 b = mux.Batch([0, N], [N], pi, pd)

@@ -35,8 +35,8 @@ def oracle_build_side(side: SideData, num_pages: int, seed: int, Hkv: int, d: in
 
 def dense_attention(side: SideData, Hq: int, Hkv: int, d: int, scale: float):
     """Numpy float64 DENSE brute force (independent of paging): gather K/V by logical
-    position from the raw rows, explicit -inf mask above the bottom-right-aligned diagonal,
-    softmax(Q K^T scale) V.  Returns (out [Σn, Hq, d], lse [Σn, Hq])."""
+    position from the raw rows (V as the cache stores it, fp16: R25), explicit -inf mask above the
+    bottom-right-aligned diagonal, softmax(Q K^T scale) V.  Returns (out [Σn, Hq, d], lse [Σn, Hq])."""
     g = Hq // Hkv
     outs, lses = [], []
     q_all = oracle.bf16_to_double(side.q)
@@ -45,7 +45,8 @@ def dense_attention(side: SideData, Hq: int, Hkv: int, d: int, scale: float):
         r, n = side.spec.r[b], side.spec.n[b]
         L = r + n
         K = oracle.bf16_to_double(side.k_rows[b])          # [L, Hkv, d]
-        V = oracle.bf16_to_double(side.v_rows[b])
+        # the V cache holds fp16 (R25): numpy's round-to-nearest-even, +-65504 clamp
+        V = np.clip(oracle.bf16_to_double(side.v_rows[b]), -65504, 65504).astype(np.float16).astype(np.float64)
         K = np.repeat(K, g, axis=1)                           # repeat_kv: q head h -> kv head h // g
         V = np.repeat(V, g, axis=1)
         Q = q_all[row0:row0 + n]                              # [n, Hq, d]

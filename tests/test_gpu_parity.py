@@ -292,8 +292,8 @@ def test_empty_and_invalid_inputs_rejected(mux):
 
 
 def test_prefill_v_range_flag(mux):
-    """The prefill P.V product runs in fp16: normal data leaves the
-    pool's error word clear; a |V| >= 65536 sets MUX_POOL_ERR_V_RANGE instead of failing silently."""
+    """The V cache is fp16 (R25, 'P precision'): normal data leaves the pool's error word
+    clear; appending a |V| >= 65536 sets MUX_POOL_ERR_V_RANGE instead of failing silently."""
     import torch
     side = _side(60, SideSpec([10], [100]), 4, 2, 128)
     o, _, ref, _, gs = _run(mux, side, 4, 2, 128, decode=False)

@@ -270,7 +270,31 @@ def test_append_byte_image_matches_naive_loop():
                 for c in range(d):
                     kref[s // 16, h, s % 16, c] = side.k_rows[b][t, h, c]
     np.testing.assert_array_equal(st["kpool"], kref)
-    assert (st["vpool"] == 0x7FC0).sum() == (kref == 0x7FC0).sum()
+    # V: the same slots, stored as fp16 (R25): numpy's float32 -> float16 (round to nearest even)
+    vref = np.full((12, Hkv, 16, d), 0x7FC0, np.uint16)
+    for b in range(3):
+        pages = list(pids[pind[b]:pind[b + 1]])
+        for t in range(side.spec.L[b]):
+            s = slot_of(pages, t)
+            vref[s // 16, :, s % 16, :] = synth.bf16_bits_to_f32(side.v_rows[b][t]).astype(np.float16).view(np.uint16)
+    np.testing.assert_array_equal(st["vpool"], vref)
+
+
+def test_v_fp16_storage_is_exact_for_bf16_inputs():
+    """R25: every bf16 value in fp16's normal range [2^-14, 65504] survives the V cache exactly, and
+    larger magnitudes clamp to +-65504 (a plain-C conversion in the oracle, pinned by numpy)."""
+    bits = np.arange(0, 1 << 16, dtype=np.uint32).astype(np.uint16)
+    x = synth.bf16_bits_to_f32(bits).astype(np.float64)
+    ok = np.isfinite(x) & (np.abs(x) >= 2.0 ** -14) & (np.abs(x) <= 65504)
+    n = bits.size                                  # one token per bf16 bit pattern, d = 8
+    k, v = oracle.empty_pool(n // 16, 1, 8, poison=True)
+    oracle.append(k, v, np.zeros((n, 1, 8), np.uint16), np.repeat(bits.reshape(n, 1, 1), 8, axis=2),
+                  np.array([0, n], np.int32), np.array([n], np.int32), np.array([0, n // 16], np.int32),
+                  np.arange(n // 16, dtype=np.int32))
+    got = oracle.f16_to_double(v[:, 0, :, 0].reshape(-1))
+    np.testing.assert_array_equal(got[ok], x[ok])
+    big = np.isfinite(x) & (np.abs(x) > 65504)
+    np.testing.assert_array_equal(got[big], np.sign(x[big]) * 65504.0)
 
 
 # ---------------------------------------------------------------- allocator (O1)
