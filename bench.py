@@ -412,6 +412,29 @@ def time_tc_share(mux, part, wl, split, pf_sms, reps=5):
     return 2.0 * T * wl.Hq * wl.d * wl.hidden / t / 1e12
 
 
+def time_qkv_fused(mux, wl, reps=5):
+    """f4: the fused QKV projection + RoPE + KV append of the step's prefill rows (T x hidden x
+    (Hq + 2 Hkv) d, Llama-3 RoPE), alone on the whole GPU, CUDA events.  Not part of the step (the
+    metric is the attention hot path); returns (launch seconds, FLOP per launch)."""
+    import torch
+    T, hidden = wl.pf_spec.total_new, wl.hidden
+    N = (wl.Hq + 2 * wl.Hkv) * wl.d
+    x = torch.randn((T, hidden), device="cuda").to(torch.bfloat16)
+    w = mux.mux_outproj_pack_w((torch.randn((hidden, N), device="cuda") / math.sqrt(hidden)).to(torch.bfloat16))
+    rope = mux.mux_rope_table(max(wl.pf_spec.L) + 1, wl.d, 500000.0)
+    q_out = torch.empty((T, wl.Hq, wl.d), dtype=torch.bfloat16, device="cuda")
+    run = lambda: mux.mux_qkv_rope_append(wl.pool, 0, wl.pf_batch, wl.Hq, x, w, rope, q_out)  # noqa: E731
+    run()
+    torch.cuda.synchronize()
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    a.record()
+    for _ in range(reps):
+        run()
+    b.record()
+    torch.cuda.synchronize()
+    return a.elapsed_time(b) / reps * 1e-3, 2.0 * T * hidden * N
+
+
 def host_cpu_model():
     try:
         out = subprocess.run(["lscpu"], capture_output=True, text=True, timeout=10).stdout
@@ -748,6 +771,14 @@ def main():
     bw_part_mux = probe_read_bw_contended(mux, part, wl, i, best["dec_sms"], step_sides[0][0])
     tc_kp = time_tc_share(mux, part, wl, i, best["pf_sms"])
     t_pf_k = time_kernel_alone(mux, part, wl, i, "pf")
+    qkv = None
+    if wl.d == 128 and wl.Hq % 2 == 0 and wl.Hkv % 2 == 0:
+        t_qkv, f_qkv = time_qkv_fused(mux, wl)
+        qkv = {"kernel": "outproj2_kernel<QKV> (tcgen05 CTA pairs, RoPE + pool-slot epilogue)",
+               "shape": f"{wl.pf_spec.total_new}x{wl.hidden}x{(wl.Hq + 2 * wl.Hkv) * wl.d}", "launch_us": t_qkv * 1e6,
+               "achieved": f_qkv / t_qkv / 1e12, "unit": "TFLOP/s", "peak": burst,
+               "frac": f_qkv / t_qkv / 1e12 / burst, "peak_src": f"{peaks_src} bf16_tflops (burst), whole GPU",
+               "note": "f4 first part, timed alone after the steps; not in the step (attention-path metric)"}
     t_dc_k = time_kernel_alone(mux, part, wl, i, "dc")
     peak_pf = burst * pf_share
     roofline = {"bound": "tensor", "kernel": "prefill6_kernel (tcgen05 causal prefill attention, 1 launch per layer)",
@@ -805,6 +836,7 @@ def main():
         "time_sliced_tok_s": step_tokens(D) / (full_pf + full_dc * D / NT),
         "sweep": sweep,
         "partition_mem_bytes": part.memory_bytes(),
+        "qkv_fused": qkv,
     }
     if hot is not None:
         line["value_hot"] = hot

@@ -2,7 +2,8 @@
 
 Plain double-precision CPU reference of the MuxWise hot path (arXiv 2504.14489):
 paged append (O2), prefill/decode attention over the paged pool (O3/O4), split
-combine (O5), out-projection (O6) and the page allocator (O1, oracle/alloc.py).
+combine (O5), out-projection (O6), the page allocator (O1, oracle/alloc.py) and the
+QKV projection + RoPE of f4 (qkv_rope).
 
 Only tests/, __graft_entry__.smoke() and bench.py (cpu_baseline leg, --impl reference)
 may import this package.  The product path (paper_2504_14489_b200) never imports it and
@@ -43,6 +44,8 @@ def lib():
                                        P, P, P, P, dbl, P, i64, P, P]
         L.oracle_partial.argtypes = [P, P, P, ctypes.c_int, ctypes.c_int, ctypes.c_int, P, dbl, i64, i64, P, P, P]
         L.oracle_combine.argtypes = [ctypes.c_int, ctypes.c_int, P, P, P, P, P]
+        L.oracle_qkv_rope.argtypes = [P, i64, ctypes.c_int, P, ctypes.c_int, ctypes.c_int, ctypes.c_int, P, dbl, P]
+        L.oracle_qkv_rope.restype = ctypes.c_int
         L.oracle_num_threads.restype = ctypes.c_int
         for f in (L.oracle_append, L.oracle_attention, L.oracle_partial, L.oracle_combine):
             f.restype = ctypes.c_int
@@ -138,6 +141,18 @@ def outproj(o_rows: np.ndarray, w_o_bits: np.ndarray) -> np.ndarray:
 
 def f16_to_double(bits: np.ndarray) -> np.ndarray:
     return np.ascontiguousarray(bits, dtype=np.uint16).view(np.float16).astype(np.float64)
+
+
+def qkv_rope(x_bits: np.ndarray, w_bits: np.ndarray, Hq: int, Hkv: int, d: int, pos, theta: float) -> np.ndarray:
+    """f4: y = x . w (float64) with RoPE(pos) on the query and key heads (R26).
+    x_bits [T][hidden], w_bits [hidden][(Hq + 2 Hkv) d] bf16 bits.  Returns float64 [T][(Hq+2Hkv) d]."""
+    x_bits, w_bits = _c(x_bits, np.uint16), _c(w_bits, np.uint16)
+    T, hidden = x_bits.shape
+    assert w_bits.shape == (hidden, (Hq + 2 * Hkv) * d)
+    pos = _c(pos, np.int32)
+    out = np.zeros((T, (Hq + 2 * Hkv) * d), np.float64)
+    lib().oracle_qkv_rope(_p(x_bits), T, hidden, _p(w_bits), Hq, Hkv, d, _p(pos), float(theta), _p(out))
+    return out
 
 
 def bf16_to_double(bits: np.ndarray) -> np.ndarray:

@@ -121,6 +121,8 @@ def lib():
         "mux_outproj_sms": [c_p, c_p, c_p, c_i32, c_i32, c_i32, c_i32, c_p, c_i32],
         "mux_outproj_pack_w": [c_p, c_p, c_i32, c_i32, c_p],
         "mux_side_plan": [ctypes.POINTER(SideC), c_i32, c_p, c_i32, ctypes.POINTER(c_i32)],
+        "mux_rope_table": [c_p, c_i32, c_i32, c_dbl, c_p],
+        "mux_qkv_rope_append": [c_p, c_i32, ctypes.POINTER(BatchC), c_i32, c_p, c_i32, c_p, c_p, c_i32, c_p, c_p],
         "mux_engine_create": [ctypes.POINTER(c_p), c_p, c_p, ctypes.POINTER(EngineDesc)],
         "mux_engine_submit": [c_p, ctypes.POINTER(RequestC), c_i32],
         "mux_engine_run": [c_p, ctypes.POINTER(EngineStats)],
@@ -472,6 +474,24 @@ def make_side(batch: Batch, num_q_heads: int, q, o, k_new=None, v_new=None, lse=
         s.attn_events = ctypes.cast(ev_arr, c_p)
     s._keep = (batch, q, o, k_new, v_new, lse, ws, w_o, y, cb, ev_arr, attn_events)
     return s
+
+
+def mux_rope_table(max_pos: int, head_dim: int = 128, theta: float = 500000.0, stream=None):
+    """Device RoPE table (cos, sin) [max_pos][head_dim/2] float32 pairs for mux_qkv_rope_append."""
+    import torch
+    t = torch.empty((max_pos, head_dim // 2, 2), dtype=torch.float32, device="cuda")
+    _check(lib().mux_rope_table(_ptr(t), max_pos, head_dim, float(theta), _stream(stream)))
+    return t
+
+
+def mux_qkv_rope_append(pool: Pool, layer: int, batch: Batch, num_q_heads: int, x, w_qkv: "PackedW", rope, q_out,
+                        stream=None):
+    """f4: Y = X . W_qkv, RoPE on the q / k heads, q -> q_out (bf16), k / v -> the pool slots (one kernel)."""
+    assert isinstance(w_qkv, PackedW), "w_qkv must be packed (mux_outproj_pack_w)"
+    T, hidden = x.shape
+    assert w_qkv.K == hidden
+    _check(lib().mux_qkv_rope_append(pool.h, layer, ctypes.byref(batch.c), num_q_heads, _ptr(x), hidden,
+                                     _ptr(w_qkv.data), _ptr(rope), int(rope.shape[0]), _ptr(q_out), _stream(stream)))
 
 
 def mux_side_plan(side: SideC, pool_layers: int) -> np.ndarray:

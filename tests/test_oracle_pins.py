@@ -358,3 +358,56 @@ def test_page_tables_cover_lengths():
     ind, ids = build_page_tables(pool, SideSpec([0, 0, 0, 0], [1, 16, 17, 33]).pages_needed())
     assert ind == [0, 1, 2, 4, 7]
     assert len(set(ids)) == len(ids)
+
+
+# ---------------------------------------------------------------- f4: QKV projection + RoPE (R26)
+def _qkv_inputs(seed, T=5, hidden=96, Hq=4, Hkv=2, d=128):
+    g = synth.rng(seed, synth.T_WO)
+    x = synth.bf16_normal(g, (T, hidden))
+    w = synth.bf16_normal(g, (hidden, (Hq + 2 * Hkv) * d), std=1 / np.sqrt(hidden))
+    return x, w
+
+
+def test_qkv_rope_position_zero_is_the_plain_projection():
+    """RoPE at position 0 is the identity, so the oracle is X . W (numpy float64 matmul)."""
+    x, w = _qkv_inputs(1)
+    out = oracle.qkv_rope(x, w, 4, 2, 128, np.zeros(5, np.int32), 500000.0)
+    ref = oracle.bf16_to_double(x) @ oracle.bf16_to_double(w)
+    np.testing.assert_allclose(out, ref, rtol=1e-12, atol=1e-12)
+
+
+def test_qkv_rope_rotation_closed_forms():
+    """Llama rotate-half convention: pair c rotates by pos * theta^(-2c/d); pair 0 turns by exactly
+    pos radians; value heads are not rotated; every pair keeps its norm."""
+    Hq, Hkv, d = 4, 2, 128
+    x, w = _qkv_inputs(2, Hq=Hq, Hkv=Hkv)
+    pos = np.array([1, 7, 100, 4095, 32767], np.int32)
+    y = oracle.bf16_to_double(x) @ oracle.bf16_to_double(w)
+    out = oracle.qkv_rope(x, w, Hq, Hkv, d, pos, 500000.0)
+    for t in range(5):
+        for h in range(Hq + Hkv):
+            a, b = y[t, h * d:h * d + 64], y[t, h * d + 64:(h + 1) * d]
+            oa, ob = out[t, h * d:h * d + 64], out[t, h * d + 64:(h + 1) * d]
+            np.testing.assert_allclose(oa ** 2 + ob ** 2, a ** 2 + b ** 2, rtol=1e-10, atol=1e-12)
+            p = float(pos[t])
+            assert abs(oa[0] - (a[0] * math.cos(p) - b[0] * math.sin(p))) < 1e-9      # pair 0: omega = 1
+            assert abs(ob[0] - (b[0] * math.cos(p) + a[0] * math.sin(p))) < 1e-9
+            w1 = 500000.0 ** (-2.0 / d)                                                   # pair 1
+            assert abs(oa[1] - (a[1] * math.cos(p * w1) - b[1] * math.sin(p * w1))) < 1e-9
+    v0 = (Hq + Hkv) * d
+    np.testing.assert_allclose(out[:, v0:], y[:, v0:], rtol=1e-12, atol=1e-12)
+
+
+def test_qkv_rope_scores_depend_on_relative_position_only():
+    """The defining property of rotary embeddings: q(m) . k(n) depends on m - n only (same token
+    contents at (m, n) and (m + s, n + s) give the same score)."""
+    Hq, Hkv, d = 2, 2, 128
+    x, w = _qkv_inputs(3, T=2, Hq=Hq, Hkv=Hkv)
+    xs = np.concatenate([x, x, x], axis=0)                  # rows: (q tok, k tok) at 3 offsets
+    pos = np.array([10, 3, 10 + 500, 3 + 500, 10 + 30000, 3 + 30000], np.int32)
+    out = oracle.qkv_rope(np.concatenate([xs[0::2][:, None], xs[1::2][:, None]], 1).reshape(6, -1), w, Hq, Hkv,
+                          d, pos, 500000.0)
+    q = out[0::2, 0:d]                                      # query head 0 of the q token
+    k = out[1::2, Hq * d:Hq * d + d]                        # key head 0 of the k token
+    s = (q * k).sum(axis=1)
+    np.testing.assert_allclose(s, s[0], rtol=1e-9, atol=1e-9)
