@@ -435,6 +435,98 @@ def time_qkv_fused(mux, wl, reps=5):
     return a.elapsed_time(b) / reps * 1e-3, 2.0 * T * hidden * N
 
 
+def time_ffn(mux, wl, inter=14336, reps=3):
+    """f4: the layer's SwiGLU FFN (Llama-3-8B width: inter 14336) on the step's prefill rows, alone
+    on the whole GPU, CUDA events.  Returns (seconds per call, FLOP per call)."""
+    import torch
+    T, hidden = wl.pf_spec.total_new, wl.hidden
+    x = torch.randn((T, hidden), device="cuda").to(torch.bfloat16)
+    w1 = (torch.randn((hidden, inter), device="cuda") / math.sqrt(hidden)).to(torch.bfloat16)
+    w3 = (torch.randn((hidden, inter), device="cuda") / math.sqrt(hidden)).to(torch.bfloat16)
+    w13 = mux.mux_ffn_pack_w13(w1, w3)
+    w2 = mux.mux_outproj_pack_w((torch.randn((inter, hidden), device="cuda") / math.sqrt(inter)).to(torch.bfloat16))
+    del w1, w3
+    h = torch.empty((T, inter), dtype=torch.bfloat16, device="cuda")
+    y = torch.empty((T, hidden), dtype=torch.bfloat16, device="cuda")
+    mux.mux_ffn_swiglu(x, w13, w2, h, y)
+    torch.cuda.synchronize()
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    a.record()
+    for _ in range(reps):
+        mux.mux_ffn_swiglu(x, w13, w2, h, y)
+    b.record()
+    torch.cuda.synchronize()
+    return a.elapsed_time(b) / reps * 1e-3, 6.0 * T * hidden * inter
+
+
+def model_step(mux, part, wl, NT, tbt_slo_ms, total_sms, inter=14336, reps=3):
+    """f4: the FULL transformer layer on both sides (fused QKV projection + RoPE + KV append ->
+    attention -> out-projection -> SwiGLU FFN, Llama-3-8B widths; norms and residual adds, which are
+    elementwise, not modelled), multiplexed like the attention step: a few decode-SM splits, D
+    decode layers balancing the isolated side times, the fastest split meeting the TBT SLO.
+    Reports model tok/s (the same token accounting as `value`)."""
+    import torch
+    T, B, hidden = wl.pf_spec.total_new, wl.dc_spec.num_seqs, wl.hidden
+    N = (wl.Hq + 2 * wl.Hkv) * wl.d
+    dev = "cuda"
+    w_qkv = mux.mux_outproj_pack_w((torch.randn((hidden, N), device=dev) / math.sqrt(hidden)).to(torch.bfloat16))
+    w1 = (torch.randn((hidden, inter), device=dev) / math.sqrt(hidden)).to(torch.bfloat16)
+    w3 = (torch.randn((hidden, inter), device=dev) / math.sqrt(hidden)).to(torch.bfloat16)
+    w13 = mux.mux_ffn_pack_w13(w1, w3)
+    del w1, w3
+    w2 = mux.mux_outproj_pack_w((torch.randn((inter, hidden), device=dev) / math.sqrt(inter)).to(torch.bfloat16))
+    rope = mux.mux_rope_table(max(max(wl.pf_spec.L), max(wl.dc_spec.L)) + 1, wl.d, 500000.0)
+    bufs = {k: (torch.randn((n, hidden), device=dev).to(torch.bfloat16), torch.empty((n, inter), dtype=torch.bfloat16, device=dev),
+                torch.empty((n, hidden), dtype=torch.bfloat16, device=dev)) for k, n in (("pf", T), ("dc", B))}
+
+    def sides(dsms, D, l0=0):
+        pf, dc, _ = wl.sides(dsms, D, l0)
+        x, h, y = bufs["pf"]
+        pf = mux.make_side(wl.pf_batch, wl.Hq, wl.pf_q, wl.pf_o, scale=wl.scale, layer0=0, num_layers=NT, w_o=wl.w_o,
+                           y=wl.pf_y, allreduce=wl.ar.get(1), qkv=(x, w_qkv, rope), ffn=(w13, w2, h, y))
+        x, h, y = bufs["dc"]
+        ns = mux.mux_decode_num_splits(B, wl.Hkv, max(wl.dc_spec.L), dsms, wl.dc_spec.L, wl.d)
+        dc = mux.make_side(wl.dc_batch, wl.Hq, wl.dc_q, wl.dc_o, scale=wl.scale, layer0=l0 % NT, num_layers=D,
+                           num_splits=ns, ws=wl.ws, w_o=wl.w_o, y=wl.dc_y, allreduce=wl.ar.get(0),
+                           qkv=(x, w_qkv, rope), ffn=(w13, w2, h, y))
+        return pf, dc
+
+    def timed(i, pf, dc, n=reps):
+        st = torch.cuda.current_stream()
+        times = torch.zeros(4, dtype=torch.int64, device=dev)
+        mux.mux_run_layer(part, i, wl.pool, pf, dc, times)
+        torch.cuda.synchronize()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(st)
+        for _ in range(n):
+            mux.mux_run_layer(part, i, wl.pool, pf, dc, times)
+        b.record(st)
+        torch.cuda.synchronize()
+        return a.elapsed_time(b) / n * 1e-3
+
+    res = []
+    for i in range(part.n):
+        dsms = part.query(i)[0]
+        if dsms not in (16, 32, 48, 64):
+            continue
+        pf, dc = sides(dsms, NT)
+        t_pf, t_dc = timed(i, pf, None, 2), timed(i, None, dc, 2)
+        D = max(1, int(round(NT * t_pf / t_dc)))
+        pf, dc = sides(dsms, D)
+        t = timed(i, pf, dc)
+        res.append({"dec_sms": dsms, "dc_layers": D, "t_ms": t * 1e3, "tbt_ms": t * 1e3 * NT / D,
+                    "tok_s": (T + B * D / NT) / t, "t_pf_iso_ms": t_pf * 1e3, "t_dc_iter_iso_ms": t_dc * 1e3})
+    ok = [r for r in res if r["tbt_ms"] <= tbt_slo_ms] or res
+    best = max(ok, key=lambda r: r["tok_s"])
+    pf, dc = sides(best["dec_sms"], NT)
+    t_full = timed(-1, pf, None, 2) + timed(-1, None, dc, 2) * best["dc_layers"] / NT
+    return {"value": best["tok_s"], "unit": "model tok/s", "split": {"dec_sms": best["dec_sms"],
+            "pf_sms": total_sms - best["dec_sms"]}, "decode_layers_per_step": best["dc_layers"],
+            "tbt_ms": best["tbt_ms"], "time_sliced_tok_s": (T + B * best["dc_layers"] / NT) / t_full, "sweep": res,
+            "layer": "fused QKV + RoPE + KV append, attention, out-projection, SwiGLU FFN (inter 14336)",
+            "note": "full-layer work per step; not the headline (the metric is the attention hot path)"}
+
+
 def host_cpu_model():
     try:
         out = subprocess.run(["lscpu"], capture_output=True, text=True, timeout=10).stdout
@@ -514,6 +606,7 @@ def main():
     ap.add_argument("--tbt-slo-ms", type=float, default=0.0,
                     help="decode TBT SLO the chosen split must meet (default: P:734, 50 ms for Llama3-8B "
                          "shapes, 100 ms for Llama3-70B)")
+    ap.add_argument("--no-model-step", action="store_true", help="skip the full-layer (f4) step")
     ap.add_argument("--oracle-1thread", action="store_true", help=argparse.SUPPRESS)
     args = ap.parse_args()
     args.warmup = max(3, args.warmup)
@@ -779,6 +872,13 @@ def main():
                "achieved": f_qkv / t_qkv / 1e12, "unit": "TFLOP/s", "peak": burst,
                "frac": f_qkv / t_qkv / 1e12 / burst, "peak_src": f"{peaks_src} bf16_tflops (burst), whole GPU",
                "note": "f4 first part, timed alone after the steps; not in the step (attention-path metric)"}
+    ffn = None
+    if args.config in (2, 3, 5):   # Llama-3-8B widths
+        t_ffn, f_ffn = time_ffn(mux, wl)
+        ffn = {"kernel": "outproj2_kernel<SwiGLU> gate/up + outproj2_kernel down (tcgen05 CTA pairs)",
+               "shape": f"T {wl.pf_spec.total_new}, hidden {wl.hidden}, inter 14336", "call_us": t_ffn * 1e6,
+               "achieved": f_ffn / t_ffn / 1e12, "unit": "TFLOP/s", "peak": burst,
+               "frac": f_ffn / t_ffn / 1e12 / burst, "note": "f4 second part, timed alone after the steps"}
     t_dc_k = time_kernel_alone(mux, part, wl, i, "dc")
     peak_pf = burst * pf_share
     roofline = {"bound": "tensor", "kernel": "prefill6_kernel (tcgen05 causal prefill attention, 1 launch per layer)",
@@ -811,6 +911,12 @@ def main():
                     "iso_achieved": wl.decode_bytes_layer() / (best["t_dc_iso_ms"] * 1e-3 / NT) / 1e9,
                     "alone_launch_us": t_dc_k * 1e6, "alone_frac_of_partition_read": wl.decode_bytes_layer() / t_dc_k
                     / 1e9 / bw_part}
+    model = None
+    if args.config in (2, 3, 5) and world == 1 and not args.no_model_step:
+        try:
+            model = model_step(mux, part, wl, NT, args.tbt_slo_ms, total_sms)
+        except Exception as e:   # reported, never silently replaced
+            model = {"error": str(e)}
     per_dc_layer = 3 + (1 if ns > 1 else 0)   # append, decode, (combine), out-proj
     launches_per_step = NT * 3 + D * per_dc_layer + 4
     line = {
@@ -836,7 +942,7 @@ def main():
         "time_sliced_tok_s": step_tokens(D) / (full_pf + full_dc * D / NT),
         "sweep": sweep,
         "partition_mem_bytes": part.memory_bytes(),
-        "qkv_fused": qkv,
+        "qkv_fused": qkv, "ffn_swiglu": ffn, "model_step": model,
     }
     if hot is not None:
         line["value_hot"] = hot

@@ -246,6 +246,23 @@ typedef struct {
    * caller with timing enabled), recorded on the side's stream right before and right after each
    * layer's attention launch(es) (decode: attention + split combine).  NULL = none. */
   void* const* attn_events;
+  /* f4 full transformer layer (optional, single GPU; the paper's layer = attention + FFN):
+   * w_qkv != NULL: each layer starts with mux_qkv_rope_append(x_in [total_q][hidden_in] bf16,
+   * w_qkv packed, rope table) writing q (the side's q buffer) and the new K/V into the pool,
+   * instead of mux_append_kv (k_new / v_new unused; append must be 0).
+   * w13 != NULL: each layer ends with mux_ffn_swiglu(y -> ffn_y, scratch ffn_h, ffn_inter) on the
+   * out-projection output (needs w_o; norms and residual adds are elementwise and not modelled).
+   * Weights are shared by all layers. */
+  const void* x_in;
+  int32_t hidden_in;
+  const void* w_qkv;
+  const void* rope;
+  int32_t rope_max_pos;
+  const void* w13;
+  const void* w2;
+  void* ffn_h;
+  void* ffn_y;
+  int32_t ffn_inter;
 } mux_side;
 
 /* Host-only dry run of a side's collective schedule (no GPU needed): for each layer i the side
@@ -313,6 +330,21 @@ int mux_rope_table(void* table, int32_t max_pos, int32_t head_dim, double theta,
 int mux_qkv_rope_append(mux_pool_t pool, int32_t layer, const mux_batch* batch, int32_t num_q_heads,
                         const void* x, int32_t hidden, const void* w_qkv_packed, const void* rope,
                         int32_t rope_max_pos, void* q_out, mux_stream_t stream);
+
+/* f4 (second part): the layer's FFN, Llama SwiGLU ("each transformer layer contains an
+ * attention layer and a feed-forward network (FFN) layer"; Table 2's FFN column, O(n d^2), P:588-590;
+ * DESIGN.md R27):  H = silu(X . W1) * (X . W3),  Y = H . W2,  silu(g) = g / (1 + e^-g).
+ * X [T][hidden] bf16, W1 / W3 [hidden][inter] bf16, W2 [inter][hidden] bf16 (packed by
+ * mux_outproj_pack_w), H [T][inter] bf16 (caller's scratch: the activation between the two GEMMs),
+ * Y [T][hidden] bf16.  The gate and up projections are ONE CTA-pair GEMM over W13 = W1 and W3
+ * interleaved in 128-column blocks (mux_ffn_pack_w13, weight prep) whose epilogue forms
+ * silu(gate) * up; the down projection is mux_outproj.  fp32 accumulation; inter % 128 == 0,
+ * hidden % 8 == 0, 16-byte aligned pointers. */
+size_t mux_ffn_w13_packed_bytes(int32_t hidden, int32_t inter);
+int mux_ffn_pack_w13(const void* w1, const void* w3, void* w13_packed, int32_t hidden, int32_t inter,
+                     mux_stream_t stream);
+int mux_ffn_swiglu(const void* x, const void* w13_packed, const void* w2_packed, void* h, void* y, int32_t T,
+                   int32_t hidden, int32_t inter, mux_stream_t stream);
 
 /* bytes of the packed layout of a [K][N] weight: ceil(N/128) * ceil(K/64) * 16384 */
 size_t mux_outproj_packed_bytes(int32_t K, int32_t N);

@@ -3,7 +3,7 @@
 Plain double-precision CPU reference of the MuxWise hot path (arXiv 2504.14489):
 paged append (O2), prefill/decode attention over the paged pool (O3/O4), split
 combine (O5), out-projection (O6), the page allocator (O1, oracle/alloc.py) and the
-QKV projection + RoPE of f4 (qkv_rope).
+QKV projection + RoPE and the SwiGLU FFN of f4 (qkv_rope, ffn_swiglu).
 
 Only tests/, __graft_entry__.smoke() and bench.py (cpu_baseline leg, --impl reference)
 may import this package.  The product path (paper_2504_14489_b200) never imports it and
@@ -46,6 +46,8 @@ def lib():
         L.oracle_combine.argtypes = [ctypes.c_int, ctypes.c_int, P, P, P, P, P]
         L.oracle_qkv_rope.argtypes = [P, i64, ctypes.c_int, P, ctypes.c_int, ctypes.c_int, ctypes.c_int, P, dbl, P]
         L.oracle_qkv_rope.restype = ctypes.c_int
+        L.oracle_ffn_swiglu.argtypes = [P, i64, ctypes.c_int, P, P, P, ctypes.c_int, P, P]
+        L.oracle_ffn_swiglu.restype = ctypes.c_int
         L.oracle_num_threads.restype = ctypes.c_int
         for f in (L.oracle_append, L.oracle_attention, L.oracle_partial, L.oracle_combine):
             f.restype = ctypes.c_int
@@ -153,6 +155,19 @@ def qkv_rope(x_bits: np.ndarray, w_bits: np.ndarray, Hq: int, Hkv: int, d: int, 
     out = np.zeros((T, (Hq + 2 * Hkv) * d), np.float64)
     lib().oracle_qkv_rope(_p(x_bits), T, hidden, _p(w_bits), Hq, Hkv, d, _p(pos), float(theta), _p(out))
     return out
+
+
+def ffn_swiglu(x_bits, w1_bits, w3_bits, w2_bits):
+    """f4 FFN (R27): h = silu(x.w1) * (x.w3) (float64), y = bf16(h) . w2.  Returns (h, y) float64."""
+    x_bits = _c(x_bits, np.uint16)
+    w1_bits, w3_bits, w2_bits = _c(w1_bits, np.uint16), _c(w3_bits, np.uint16), _c(w2_bits, np.uint16)
+    T, hidden = x_bits.shape
+    inter = w1_bits.shape[1]
+    assert w1_bits.shape == w3_bits.shape == (hidden, inter) and w2_bits.shape == (inter, hidden)
+    h = np.zeros((T, inter), np.float64)
+    y = np.zeros((T, hidden), np.float64)
+    lib().oracle_ffn_swiglu(_p(x_bits), T, hidden, _p(w1_bits), _p(w3_bits), _p(w2_bits), inter, _p(h), _p(y))
+    return h, y
 
 
 def bf16_to_double(bits: np.ndarray) -> np.ndarray:

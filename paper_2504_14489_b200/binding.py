@@ -51,7 +51,9 @@ class SideC(ctypes.Structure):
                 ("layer0", c_i32), ("num_layers", c_i32), ("append", c_i32), ("num_splits", c_i32),
                 ("ws", c_p), ("ws_bytes", c_sz), ("w_o", c_p), ("y", c_p), ("w_stride", c_i64),
                 ("y_stride", c_i64), ("hidden", c_i32), ("y_dtype", c_i32), ("hook", LayerHook),
-                ("hook_user", c_p), ("ar_fn", c_p), ("ar_comm", c_p), ("attn_events", c_p)]
+                ("hook_user", c_p), ("ar_fn", c_p), ("ar_comm", c_p), ("attn_events", c_p),
+                ("x_in", c_p), ("hidden_in", c_i32), ("w_qkv", c_p), ("rope", c_p), ("rope_max_pos", c_i32),
+                ("w13", c_p), ("w2", c_p), ("ffn_h", c_p), ("ffn_y", c_p), ("ffn_inter", c_i32)]
 
 
 class EngineDesc(ctypes.Structure):
@@ -122,6 +124,8 @@ def lib():
         "mux_outproj_pack_w": [c_p, c_p, c_i32, c_i32, c_p],
         "mux_side_plan": [ctypes.POINTER(SideC), c_i32, c_p, c_i32, ctypes.POINTER(c_i32)],
         "mux_rope_table": [c_p, c_i32, c_i32, c_dbl, c_p],
+        "mux_ffn_pack_w13": [c_p, c_p, c_p, c_i32, c_i32, c_p],
+        "mux_ffn_swiglu": [c_p, c_p, c_p, c_p, c_p, c_i32, c_i32, c_i32, c_p],
         "mux_qkv_rope_append": [c_p, c_i32, ctypes.POINTER(BatchC), c_i32, c_p, c_i32, c_p, c_p, c_i32, c_p, c_p],
         "mux_engine_create": [ctypes.POINTER(c_p), c_p, c_p, ctypes.POINTER(EngineDesc)],
         "mux_engine_submit": [c_p, ctypes.POINTER(RequestC), c_i32],
@@ -428,7 +432,7 @@ def mux_partition_create(device: int, decode_sms: Sequence[int]) -> Partition:
 def make_side(batch: Batch, num_q_heads: int, q, o, k_new=None, v_new=None, lse=None, scale: float = 1.0,
               layer0: int = 0, num_layers: int = 1, append: bool = False, num_splits: int = 0, ws=None,
               per_layer_inputs: bool = False, w_o=None, y=None, hook=None, allreduce=None,
-              attn_events=None) -> SideC:
+              attn_events=None, qkv=None, ffn=None) -> SideC:
     """Build a mux_side.  per_layer_inputs: q/k_new/v_new/o/lse carry a leading layer dim
     and layer i uses slice i (stride = one slice); otherwise every layer reuses the buffers.
     allreduce: (fn address, comm handle) of the NCCL all-reduce the library enqueues after every
@@ -472,7 +476,15 @@ def make_side(batch: Batch, num_q_heads: int, q, o, k_new=None, v_new=None, lse=
         assert len(attn_events) >= 2 * num_layers
         ev_arr = (c_p * len(attn_events))(*attn_events.handles())
         s.attn_events = ctypes.cast(ev_arr, c_p)
-    s._keep = (batch, q, o, k_new, v_new, lse, ws, w_o, y, cb, ev_arr, attn_events)
+    if qkv is not None:   # f4: (x_in, w_qkv PackedW, rope table) -> fused projection + RoPE + append
+        x_in, w_qkv, rope = qkv
+        s.x_in, s.hidden_in, s.w_qkv = _ptr(x_in), int(x_in.shape[1]), _ptr(w_qkv.data)
+        s.rope, s.rope_max_pos = _ptr(rope), int(rope.shape[0])
+        s.append = 0
+    if ffn is not None:   # f4: (w13 PackedW, w2 PackedW, h scratch, y_ffn) -> SwiGLU FFN after out-proj
+        w13, w2, fh, fy = ffn
+        s.w13, s.w2, s.ffn_h, s.ffn_y, s.ffn_inter = _ptr(w13.data), _ptr(w2.data), _ptr(fh), _ptr(fy), int(w13.N // 2)
+    s._keep = (batch, q, o, k_new, v_new, lse, ws, w_o, y, cb, ev_arr, attn_events, qkv, ffn)
     return s
 
 
@@ -492,6 +504,29 @@ def mux_qkv_rope_append(pool: Pool, layer: int, batch: Batch, num_q_heads: int, 
     assert w_qkv.K == hidden
     _check(lib().mux_qkv_rope_append(pool.h, layer, ctypes.byref(batch.c), num_q_heads, _ptr(x), hidden,
                                      _ptr(w_qkv.data), _ptr(rope), int(rope.shape[0]), _ptr(q_out), _stream(stream)))
+
+
+def mux_ffn_pack_w13(w1, w3, stream=None) -> "PackedW":
+    """Weight prep of the SwiGLU FFN: W1 and W3 [hidden][inter] bf16 interleaved in 128-column blocks
+    and packed (mux_ffn_pack_w13) -> PackedW of [hidden][2 inter]."""
+    import torch
+    hidden, inter = w1.shape
+    assert tuple(w3.shape) == (hidden, inter)
+    lib().mux_ffn_w13_packed_bytes.restype = c_sz
+    nbytes = lib().mux_ffn_w13_packed_bytes(hidden, inter)
+    out = torch.empty((1, nbytes), dtype=torch.uint8, device="cuda")
+    _check(lib().mux_ffn_pack_w13(_ptr(w1), _ptr(w3), _ptr(out), hidden, inter, _stream(stream)))
+    return PackedW(out, hidden, 2 * inter)
+
+
+def mux_ffn_swiglu(x, w13: "PackedW", w2: "PackedW", h, y, stream=None):
+    """f4 FFN: h = silu(x W1) * (x W3) (one GEMM + epilogue), y = h W2."""
+    T, hidden = x.shape
+    inter = w13.N // 2
+    assert w13.K == hidden and w2.K == inter and w2.N == hidden
+    assert tuple(h.shape) == (T, inter) and tuple(y.shape) == (T, hidden)
+    _check(lib().mux_ffn_swiglu(_ptr(x), _ptr(w13.data), _ptr(w2.data), _ptr(h), _ptr(y), T, hidden, inter,
+                                _stream(stream)))
 
 
 def mux_side_plan(side: SideC, pool_layers: int) -> np.ndarray:

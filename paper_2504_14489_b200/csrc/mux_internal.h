@@ -72,6 +72,11 @@ int run_side(mux_pool_t pool, const mux_side* s, bool decode, int sms, cudaStrea
              unsigned long long* t1);
 void launch_stamp(unsigned long long* dst, cudaStream_t st);
 // outproj.cu: mux_outproj with the SM count of the launching partition (persistent grid)
+int qkv_launch(mux_pool_t pool, int32_t layer, const mux_batch* b, int32_t hq, const void* x, int32_t hidden,
+               const void* w_qkv, const void* rope, int32_t rope_max_pos, void* q_out, mux_stream_t stream,
+               int num_sms);
+int ffn_launch(const void* x, const void* w13_packed, const void* w2_packed, void* h, void* y, int32_t T,
+               int32_t hidden, int32_t inter, mux_stream_t stream, int num_sms);
 int outproj_launch(const void* x, const void* w, void* y, int32_t y_dtype, int32_t T, int32_t K, int32_t N,
                    mux_stream_t stream, int num_sms);
 

@@ -253,7 +253,8 @@ struct Gemm2Smem {
   static constexpr int kBytes = kTmemSlot + 16;
 };
 
-template <bool QKV>
+// EPI: 0 = plain Y store, 1 = fused QKV + RoPE + append (f4), 2 = SwiGLU gate/up (f4 FFN)
+template <int EPI>
 __global__ void __launch_bounds__(kGThreads, 1)
     outproj2_kernel(const __grid_constant__ CUtensorMap tmap_x, const __grid_constant__ CUtensorMap tmap_w,
                     const GemmParams p, const QkvParams qp) {
@@ -334,7 +335,47 @@ __global__ void __launch_bounds__(kGThreads, 1)
       }
     }
     __syncwarp();
-  } else if (QKV) {
+  } else if (EPI == 2) {
+    // SwiGLU epilogue (both CTAs): W13 is packed with 128-column blocks of W1 and W3 interleaved,
+    // so output tile n0 holds gate columns [n0/2, n0/2 + 128) then the matching up columns;
+    // h = silu(gate) * up -> H[row][n0/2 + c] (bf16, row stride p.N / 2 = inter)
+    int i = 0;
+    for (int t = pair; t < tiles; t += npairs, ++i) {
+      const int b = i & 1;
+      const int m0 = (t / p.n_tiles) * 2 * kGBM + static_cast<int>(rank) * kGBM;
+      const int n0 = (t % p.n_tiles) * kGBN;
+      dev::mbar_wait_sleep(&acc_full[b], (i >> 1) & 1);
+      dev::tc_fence_after();
+      const int row = m0 + warp * 32 + lane;
+      const uint32_t taddr = tmem + b * kGBN + (static_cast<uint32_t>(warp * 32) << 16);
+#pragma unroll 1
+      for (int c = 0; c < 4; ++c) {
+        uint32_t g[32], u[32];
+        dev::tmem_ld32(taddr + c * 32, g);
+        dev::tmem_ld32(taddr + 128 + c * 32, u);
+        dev::tmem_wait_ld();
+        if (c == 3) {
+          dev::tc_fence_before();
+          __syncwarp();
+          if (lane == 0) dev::mbar_arrive_cluster(acc_empty_leader + b * 8);
+        }
+        if (row >= p.T) continue;
+        float hv[32];
+#pragma unroll
+        for (int k = 0; k < 32; ++k) {
+          const float gv = __uint_as_float(g[k]);
+          // silu(g) = g / (1 + e^-g)
+          hv[k] = gv / (1.f + dev::ex2(-gv * 1.4426950408889634f)) * __uint_as_float(u[k]);
+        }
+        uint4* dst = reinterpret_cast<uint4*>(static_cast<uint16_t*>(p.y) + static_cast<size_t>(row) * (p.N / 2) +
+                                              n0 / 2 + c * 32);
+#pragma unroll
+        for (int k = 0; k < 4; ++k)
+          dst[k] = make_uint4(dev::pack_bf16(hv[8 * k], hv[8 * k + 1]), dev::pack_bf16(hv[8 * k + 2], hv[8 * k + 3]),
+                              dev::pack_bf16(hv[8 * k + 4], hv[8 * k + 5]), dev::pack_bf16(hv[8 * k + 6], hv[8 * k + 7]));
+      }
+    }
+  } else if (EPI == 1) {
     // fused QKV epilogue (both CTAs): my 128 rows (tokens) x 2 heads of TMEM buffer b
     int i = 0;
     for (int t = pair; t < tiles; t += npairs, ++i) {
@@ -638,7 +679,7 @@ int outproj_launch(const void* x, const void* w, void* y, int32_t y_dtype, int32
     static bool attr2 = false;
     const int smem2 = Gemm2Smem::kBytes + 1024;
     if (!attr2) {
-      MUX_CUDA(cudaFuncSetAttribute(outproj2_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem2));
+      MUX_CUDA(cudaFuncSetAttribute(outproj2_kernel<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem2));
       attr2 = true;
     }
     GemmParams prm{y, wp, T, N, K, y_dtype == MUX_DTYPE_F32, (T + 2 * kGBM - 1) / (2 * kGBM), (N + kGBN - 1) / kGBN};
@@ -657,7 +698,7 @@ int outproj_launch(const void* x, const void* w, void* y, int32_t y_dtype, int32
     attr[0].val.clusterDim.z = 1;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
-    const cudaError_t e = cudaLaunchKernelEx(&cfg, outproj2_kernel<false>, tx, tw, prm, QkvParams{});
+    const cudaError_t e = cudaLaunchKernelEx(&cfg, outproj2_kernel<0>, tx, tw, prm, QkvParams{});
     if (e == cudaSuccess) return MUX_OK;
     (void)cudaGetLastError();  // no CTA pairs on this partition: fall back to the single-CTA kernel
   }
@@ -710,10 +751,10 @@ extern "C" int mux_rope_table(void* table, int32_t max_pos, int32_t head_dim, do
   return MUX_OK;
 }
 
-extern "C" int mux_qkv_rope_append(mux_pool_t pool, int32_t layer, const mux_batch* b, int32_t hq, const void* x,
-                                   int32_t hidden, const void* w_qkv, const void* rope, int32_t rope_max_pos,
-                                   void* q_out, mux_stream_t stream) {
-  using namespace mux;
+namespace mux {
+int qkv_launch(mux_pool_t pool, int32_t layer, const mux_batch* b, int32_t hq, const void* x, int32_t hidden,
+               const void* w_qkv, const void* rope, int32_t rope_max_pos, void* q_out, mux_stream_t stream,
+               int num_sms) {
   int rc = check_pool_layer(pool, layer);
   if (rc) return rc;
   if ((rc = validate_batch(b, false))) return rc;
@@ -744,7 +785,7 @@ extern "C" int mux_qkv_rope_append(mux_pool_t pool, int32_t layer, const mux_bat
   static bool attr = false;
   const int smem2 = Gemm2Smem::kBytes + 1024;
   if (!attr) {
-    MUX_CUDA(cudaFuncSetAttribute(outproj2_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem2));
+    MUX_CUDA(cudaFuncSetAttribute(outproj2_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem2));
     attr = true;
   }
   GemmParams prm{nullptr, static_cast<const uint8_t*>(w_qkv), T, N, K, 0, (T + 2 * kGBM - 1) / (2 * kGBM),
@@ -754,7 +795,7 @@ extern "C" int mux_qkv_rope_append(mux_pool_t pool, int32_t layer, const mux_bat
                static_cast<uint16_t*>(pool->desc.k_storage) + off, static_cast<uint16_t*>(pool->desc.v_storage) + off,
                static_cast<uint16_t*>(q_out), static_cast<const float2*>(rope), rope_max_pos, hq, hkv, pool->d_err};
   const int tiles = prm.m_tiles * prm.n_tiles;
-  const int pairs = std::max(1, std::min(tiles, device_sm_count() / 2));
+  const int pairs = std::max(1, std::min(tiles, (num_sms > 0 ? num_sms : device_sm_count()) / 2));
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3(2 * pairs);
   cfg.blockDim = dim3(kGThreads);
@@ -767,8 +808,113 @@ extern "C" int mux_qkv_rope_append(mux_pool_t pool, int32_t layer, const mux_bat
   at[0].val.clusterDim.z = 1;
   cfg.attrs = at;
   cfg.numAttrs = 1;
-  MUX_CUDA(cudaLaunchKernelEx(&cfg, outproj2_kernel<true>, tx, tw, prm, qp));
+  MUX_CUDA(cudaLaunchKernelEx(&cfg, outproj2_kernel<1>, tx, tw, prm, qp));
   return MUX_OK;
+}
+}  // namespace mux
+
+extern "C" int mux_qkv_rope_append(mux_pool_t pool, int32_t layer, const mux_batch* b, int32_t hq, const void* x,
+                                   int32_t hidden, const void* w_qkv, const void* rope, int32_t rope_max_pos,
+                                   void* q_out, mux_stream_t stream) {
+  return mux::qkv_launch(pool, layer, b, hq, x, hidden, w_qkv, rope, rope_max_pos, q_out, stream, 0);
+}
+
+// ---------------------------------------------------------------- f4: SwiGLU FFN (gate/up fused)
+namespace mux {
+namespace {
+// W13 [K][2 inter] with 128-column blocks of W1 and W3 interleaved, written in the packed tile image
+__global__ void pack_w13_kernel(const uint16_t* __restrict__ w1, const uint16_t* __restrict__ w3,
+                                uint4* __restrict__ out, int K, int inter, int KB, size_t nchunks) {
+  for (size_t i = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; i < nchunks;
+       i += static_cast<size_t>(gridDim.x) * blockDim.x) {
+    const int pos = static_cast<int>(i & 7);
+    const int k = static_cast<int>((i >> 3) & 63);
+    const int half = static_cast<int>((i >> 9) & 1);
+    const size_t tile = i >> 10;
+    const int kb = static_cast<int>(tile % KB), nt = static_cast<int>(tile / KB);
+    const int c = pos ^ (k & 7);
+    const int n = nt * 128 + half * 64 + c * 8, kk = kb * kGBK + k;   // column of W13
+    const uint16_t* src = (n / 128) & 1 ? w3 : w1;                     // odd 128-blocks: W3
+    const int col = (n / 256) * 128 + (n % 128);
+    uint4 v = make_uint4(0, 0, 0, 0);
+    if (kk < K && col < inter) v = *reinterpret_cast<const uint4*>(src + static_cast<size_t>(kk) * inter + col);
+    out[i] = v;
+  }
+}
+}  // namespace
+}  // namespace mux
+
+extern "C" size_t mux_ffn_w13_packed_bytes(int32_t hidden, int32_t inter) {
+  return mux_outproj_packed_bytes(hidden, 2 * inter);
+}
+
+extern "C" int mux_ffn_pack_w13(const void* w1, const void* w3, void* w13_packed, int32_t hidden, int32_t inter,
+                                mux_stream_t stream) {
+  using namespace mux;
+  if (!w1 || !w3 || !w13_packed) return fail(MUX_ERR_INVALID_ARG, "mux_ffn_pack_w13: NULL pointer");
+  if (hidden < 1 || inter < 128 || inter % 128) return fail(MUX_ERR_UNSUPPORTED, "mux_ffn_pack_w13: inter % 128 == 0");
+  if ((reinterpret_cast<uintptr_t>(w1) | reinterpret_cast<uintptr_t>(w3) | reinterpret_cast<uintptr_t>(w13_packed)) & 15)
+    return fail(MUX_ERR_INVALID_ARG, "mux_ffn_pack_w13: pointers must be 16-byte aligned");
+  const size_t nchunks = mux_ffn_w13_packed_bytes(hidden, inter) / 16;
+  const int blocks = static_cast<int>(std::min<size_t>((nchunks + 255) / 256, 148 * 16));
+  pack_w13_kernel<<<blocks, 256, 0, reinterpret_cast<cudaStream_t>(stream)>>>(
+      static_cast<const uint16_t*>(w1), static_cast<const uint16_t*>(w3), static_cast<uint4*>(w13_packed), hidden,
+      inter, (hidden + kGBK - 1) / kGBK, nchunks);
+  MUX_CUDA(cudaGetLastError());
+  return MUX_OK;
+}
+
+namespace mux {
+int ffn_launch(const void* x, const void* w13_packed, const void* w2_packed, void* h, void* y, int32_t T,
+               int32_t hidden, int32_t inter, mux_stream_t stream, int num_sms) {
+  if (!x || !w13_packed || !w2_packed || !h || !y) return fail(MUX_ERR_INVALID_ARG, "mux_ffn_swiglu: NULL pointer");
+  if (T < 1 || hidden < 8 || hidden % 8 || inter < 128 || inter % 128)
+    return fail(MUX_ERR_UNSUPPORTED, "mux_ffn_swiglu: T >= 1, hidden % 8 == 0, inter % 128 == 0");
+  if ((reinterpret_cast<uintptr_t>(x) | reinterpret_cast<uintptr_t>(h) | reinterpret_cast<uintptr_t>(y)) & 15)
+    return fail(MUX_ERR_INVALID_ARG, "mux_ffn_swiglu: pointers must be 16-byte aligned");
+  const int K = hidden, N = 2 * inter;
+  CUtensorMap tx, tw;
+  uint64_t dx[3] = {static_cast<uint64_t>(K), static_cast<uint64_t>(T), 1};
+  uint64_t sx[2] = {static_cast<uint64_t>(K) * 2, static_cast<uint64_t>(K) * T * 2};
+  uint32_t bx[3] = {kGBK, kGBM, 1};
+  int rc;
+  if ((rc = make_tmap_bf16(&tx, x, 3, dx, sx, bx))) return rc;
+  const int KB = (K + kGBK - 1) / kGBK, NT = N / 128;
+  uint64_t dw[3] = {64, 128, static_cast<uint64_t>(KB) * NT};
+  uint64_t sw[2] = {128, 16384};
+  uint32_t bw[3] = {64, 128, 1};
+  if ((rc = make_tmap_bf16(&tw, w13_packed, 3, dw, sw, bw, false))) return rc;
+  static bool attr = false;
+  const int smem2 = Gemm2Smem::kBytes + 1024;
+  if (!attr) {
+    MUX_CUDA(cudaFuncSetAttribute(outproj2_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem2));
+    attr = true;
+  }
+  // N = 2 inter columns of W13; the epilogue writes H [T][inter] (bf16)
+  GemmParams prm{h, static_cast<const uint8_t*>(w13_packed), T, N, K, 0, (T + 2 * kGBM - 1) / (2 * kGBM), N / kGBN};
+  const int tiles = prm.m_tiles * prm.n_tiles;
+  const int pairs = std::max(1, std::min(tiles, (num_sms > 0 ? num_sms : device_sm_count()) / 2));
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(2 * pairs);
+  cfg.blockDim = dim3(kGThreads);
+  cfg.dynamicSmemBytes = smem2;
+  cfg.stream = reinterpret_cast<cudaStream_t>(stream);
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeClusterDimension;
+  at[0].val.clusterDim.x = 2;
+  at[0].val.clusterDim.y = 1;
+  at[0].val.clusterDim.z = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  MUX_CUDA(cudaLaunchKernelEx(&cfg, outproj2_kernel<2>, tx, tw, prm, QkvParams{}));
+  // down projection: Y = H . W2 (the plain GEMM)
+  return outproj_launch(h, w2_packed, y, MUX_DTYPE_BF16, T, inter, hidden, stream, num_sms);
+}
+}  // namespace mux
+
+extern "C" int mux_ffn_swiglu(const void* x, const void* w13_packed, const void* w2_packed, void* h, void* y,
+                              int32_t T, int32_t hidden, int32_t inter, mux_stream_t stream) {
+  return mux::ffn_launch(x, w13_packed, w2_packed, h, y, T, hidden, inter, stream, 0);
 }
 
 extern "C" int mux_outproj(const void* x, const void* w, void* y, int32_t y_dtype, int32_t T, int32_t K, int32_t N,

@@ -176,6 +176,10 @@ int run_side(mux_pool_t pool, const mux_side* s, bool decode, int sms, cudaStrea
     return fail(MUX_ERR_INVALID_ARG, "out-projection needs bf16 o, y and hidden >= 1");
   if (s->ar_fn && (!s->w_o || !s->ar_comm || s->y_dtype != MUX_DTYPE_BF16))
     return fail(MUX_ERR_INVALID_ARG, "all-reduce needs w_o, a bf16 y and ar_comm");
+  if (s->w_qkv && (s->append || !s->x_in || !s->rope || s->hidden_in < 8))
+    return fail(MUX_ERR_INVALID_ARG, "fused QKV needs x_in, hidden_in, rope and append == 0");
+  if (s->w13 && (!s->w_o || !s->w2 || !s->ffn_h || !s->ffn_y || s->ffn_inter < 128 || s->y_dtype != MUX_DTYPE_BF16))
+    return fail(MUX_ERR_INVALID_ARG, "FFN needs w_o (bf16 y), w2, ffn_h, ffn_y and ffn_inter");
   using nccl_allreduce_t = int (*)(const void*, void*, size_t, int, int, void*, cudaStream_t);
   auto ar = reinterpret_cast<nccl_allreduce_t>(s->ar_fn);
   auto ev = [&](int i, int which) -> int {
@@ -196,6 +200,11 @@ int run_side(mux_pool_t pool, const mux_side* s, bool decode, int sms, cudaStrea
       return base ? static_cast<const void*>(static_cast<const uint8_t*>(base) + stride * i) : nullptr;
     };
     int rc;
+    if (s->w_qkv) {   // f4: projection + RoPE + append in one kernel; q is its output
+      rc = qkv_launch(pool, layer, s->batch, s->num_q_heads, s->x_in, s->hidden_in, s->w_qkv, s->rope,
+                      s->rope_max_pos, const_cast<void*>(at(s->q, s->q_stride)), reinterpret_cast<mux_stream_t>(st), sms);
+      if (rc) return rc;
+    }
     if (s->append) {
       rc = mux_append_kv(pool, layer, s->batch, at(s->k_new, s->kv_stride), at(s->v_new, s->kv_stride),
                          reinterpret_cast<mux_stream_t>(st));
@@ -221,6 +230,11 @@ int run_side(mux_pool_t pool, const mux_side* s, bool decode, int sms, cudaStrea
         const int nrc = ar(y, y, static_cast<size_t>(side_allreduce_count(s)), 9 /* ncclBfloat16 */,
                            0 /* ncclSum */, s->ar_comm, st);
         if (nrc) return fail(MUX_ERR_CUDA, "ncclAllReduce of the out-projection failed (NCCL error " + std::to_string(nrc) + ")");
+      }
+      if (s->w13) {   // f4: the layer's FFN on the attention block's output
+        rc = ffn_launch(y, s->w13, s->w2, s->ffn_h, s->ffn_y, s->batch->total_q, s->hidden, s->ffn_inter,
+                        reinterpret_cast<mux_stream_t>(st), sms);
+        if (rc) return rc;
       }
     }
     if (s->hook) s->hook(s->hook_user, decode ? 0 : 1, i, reinterpret_cast<mux_stream_t>(st));

@@ -105,3 +105,28 @@ def test_qkv_rope_rejects_positions_past_the_table(mux):
     q_out = torch.empty((20, Hq, d), dtype=torch.bfloat16, device="cuda")
     with pytest.raises(mux.MuxError):
         mux.mux_qkv_rope_append(pool, 0, batch, Hq, x, w, mux.mux_rope_table(64, d), q_out)
+
+
+@pytest.mark.parametrize("T,hidden,inter", [(300, 256, 384), (129, 1024, 2048), (64, 4096, 14336)])
+def test_ffn_swiglu_matches_oracle(mux, T, hidden, inter):
+    """f4 FFN (R27): the gate/up GEMM with its silu * up epilogue and the down GEMM against the
+    oracle: H (bf16) within one bf16 rounding of the float64 h, Y within the rounding of H plus
+    fp32 accumulation."""
+    import torch
+    g = synth.rng(12, synth.T_WO, salt=T)
+    x = synth.bf16_normal(g, (T, hidden))
+    w1 = synth.bf16_normal(g, (hidden, inter), std=1 / math.sqrt(hidden))
+    w3 = synth.bf16_normal(g, (hidden, inter), std=1 / math.sqrt(hidden))
+    w2 = synth.bf16_normal(g, (inter, hidden), std=1 / math.sqrt(inter))
+    w13 = mux.mux_ffn_pack_w13(_dev(w1), _dev(w3))
+    w2p = mux.mux_outproj_pack_w(_dev(w2))
+    h = torch.empty((T, inter), dtype=torch.bfloat16, device="cuda")
+    y = torch.empty((T, hidden), dtype=torch.bfloat16, device="cuda")
+    mux.mux_ffn_swiglu(_dev(x), w13, w2p, h, y)
+    torch.cuda.synchronize()
+    rh, ry = oracle.ffn_swiglu(x, w1, w3, w2)
+    _close(oracle.bf16_to_double(_bits(h)), rh, 2.0 ** -8, "h")
+    gy = oracle.bf16_to_double(_bits(y))
+    d = np.abs(gy - ry)
+    tol = 2.0 ** -7 * np.abs(ry) + 1e-2 * np.sqrt(np.mean(ry ** 2))
+    assert (d <= tol).all(), f"y: {(d > tol).sum()} elements out of tolerance, max|d| {d.max():.3e}"

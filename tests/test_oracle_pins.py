@@ -411,3 +411,23 @@ def test_qkv_rope_scores_depend_on_relative_position_only():
     k = out[1::2, Hq * d:Hq * d + d]                        # key head 0 of the k token
     s = (q * k).sum(axis=1)
     np.testing.assert_allclose(s, s[0], rtol=1e-9, atol=1e-9)
+
+
+# ---------------------------------------------------------------- f4: SwiGLU FFN (R27)
+def test_ffn_swiglu_matches_numpy_and_closed_forms():
+    """h = silu(x W1) * (x W3) against numpy (scipy's expit as the sigmoid), y = bf16(h) W2 against a
+    numpy matmul of the rounded h; silu(0) = 0 and silu(a) -> a for large a."""
+    import scipy.special
+    g = synth.rng(4, synth.T_WO)
+    T, hidden, inter = 6, 64, 256
+    x = synth.bf16_normal(g, (T, hidden))
+    w1, w3 = synth.bf16_normal(g, (hidden, inter), std=0.2), synth.bf16_normal(g, (hidden, inter), std=0.2)
+    w2 = synth.bf16_normal(g, (inter, hidden), std=0.1)
+    h, y = oracle.ffn_swiglu(x, w1, w3, w2)
+    a = oracle.bf16_to_double(x) @ oracle.bf16_to_double(w1)
+    b = oracle.bf16_to_double(x) @ oracle.bf16_to_double(w3)
+    np.testing.assert_allclose(h, a * scipy.special.expit(a) * b, rtol=1e-12, atol=1e-12)
+    hb = oracle.bf16_to_double(synth.f32_to_bf16_bits(h.astype(np.float32)))
+    np.testing.assert_allclose(y, hb @ oracle.bf16_to_double(w2), rtol=1e-9, atol=1e-9)
+    z = np.zeros((1, hidden), np.uint16)                      # x = 0 -> silu(0) * 0 = 0
+    assert not oracle.ffn_swiglu(z, w1, w3, w2)[1].any()
