@@ -130,3 +130,61 @@ def test_ffn_swiglu_matches_oracle(mux, T, hidden, inter):
     d = np.abs(gy - ry)
     tol = 2.0 ** -7 * np.abs(ry) + 1e-2 * np.sqrt(np.mean(ry ** 2))
     assert (d <= tol).all(), f"y: {(d > tol).sum()} elements out of tolerance, max|d| {d.max():.3e}"
+
+
+@pytest.mark.parametrize("decode", [False, True])
+def test_full_layer_side_equals_the_composed_calls(mux, decode):
+    """mux_side's full-layer mode (fused QKV + RoPE + append -> attention -> out-projection ->
+    FFN per layer) through mux_run_layer gives bitwise the outputs of the same steps called one by
+    one (each of which is checked against the oracle above and in test_gpu_parity.py)."""
+    import torch
+    Hq, Hkv, d, hidden, inter, layers = 8, 2, 128, 256, 384, 2
+    spec = SideSpec([33, 0, 200], [1, 1, 1]) if decode else SideSpec([0, 40], [150, 77])
+    T = spec.total_new
+    g = synth.rng(13, synth.T_WO, salt=int(decode))
+    x = _dev(synth.bf16_normal(g, (T, hidden)))
+    w_qkv = mux.mux_outproj_pack_w(_dev(synth.bf16_normal(g, (hidden, (Hq + 2 * Hkv) * d), std=0.06)))
+    w_o = mux.mux_outproj_pack_w(_dev(synth.bf16_normal(g, (Hq * d, hidden), std=0.03)))
+    w13 = mux.mux_ffn_pack_w13(_dev(synth.bf16_normal(g, (hidden, inter), std=0.06)),
+                               _dev(synth.bf16_normal(g, (hidden, inter), std=0.06)))
+    w2 = mux.mux_outproj_pack_w(_dev(synth.bf16_normal(g, (inter, hidden), std=0.05)))
+    rope = mux.mux_rope_table(max(spec.L) + 1, d)
+    outs = []
+    for fused in (True, False):
+        pages = sum(spec.pages_needed()) + 4
+        kst = torch.zeros((layers, pages, Hkv, 16, d), dtype=torch.bfloat16, device="cuda")
+        vst = torch.zeros((layers, pages, Hkv, 16, d), dtype=torch.float16, device="cuda")
+        pool = mux.Pool(layers, pages, Hkv, d, 9, kst, vst)
+        pind, pids = pool.page_tables(spec.pages_needed())
+        # the cached prefix of every layer (same bytes in both runs)
+        for l in range(layers):
+            kst[l].normal_(generator=torch.Generator(device="cuda").manual_seed(l))
+            vst[l].normal_(generator=torch.Generator(device="cuda").manual_seed(100 + l))
+        batch = mux.Batch(indptr(spec.n), spec.L, pind, pids)
+        q = torch.empty((T, Hq, d), dtype=torch.bfloat16, device="cuda")
+        o = torch.empty((T, Hq, d), dtype=torch.bfloat16, device="cuda")
+        y = torch.empty((T, hidden), dtype=torch.bfloat16, device="cuda")
+        h = torch.empty((T, inter), dtype=torch.bfloat16, device="cuda")
+        fy = torch.empty((T, hidden), dtype=torch.bfloat16, device="cuda")
+        ws = torch.empty(1 << 22, dtype=torch.uint8, device="cuda")
+        if fused:
+            part = mux.Partition(0, [16])
+            side = mux.make_side(batch, Hq, q, o, scale=1 / math.sqrt(d), layer0=0, num_layers=layers, w_o=w_o, y=y,
+                                 num_splits=2 if decode else 0, ws=ws if decode else None,
+                                 qkv=(x, w_qkv, rope), ffn=(w13, w2, h, fy))
+            mux.mux_run_layer(part, 0, pool, None if decode else side, side if decode else None)
+            torch.cuda.synchronize()
+            part.close()
+        else:
+            for l in range(layers):
+                mux.mux_qkv_rope_append(pool, l, batch, Hq, x, w_qkv, rope, q)
+                if decode:
+                    mux.mux_decode_attn(pool, l, batch, Hq, q, o, None, scale=1 / math.sqrt(d), num_splits=2, ws=ws)
+                else:
+                    mux.mux_prefill_attn(pool, l, batch, Hq, q, o, None, scale=1 / math.sqrt(d))
+                mux.mux_outproj(o.view(T, -1), w_o, y)
+                mux.mux_ffn_swiglu(y, w13, w2, h, fy)
+            torch.cuda.synchronize()
+        outs.append([_bits(t) for t in (q, o, y, fy, kst, vst.view(torch.bfloat16))])
+    for a, b, name in zip(outs[0], outs[1], ("q", "o", "y", "ffn y", "K pool", "V pool")):
+        np.testing.assert_array_equal(a, b, err_msg=name)
