@@ -20,10 +20,12 @@ gran = ctypes.c_size_t()
 p = Prop(1, 2 << 20, 0, 0)
 rc = cu.cuMulticastGetGranularity(ctypes.byref(gran), ctypes.byref(p), 0)
 print("granularity:", rc, gran.value)
-h = ctypes.c_ulonglong()
-p.size = max(gran.value, 2 << 20)
-rc = cu.cuMulticastCreate(ctypes.byref(h), ctypes.byref(p))
-print("cuMulticastCreate:", rc)
-if rc == 0:
-    rc = cu.cuMulticastAddDevice(h, 0)
-    print("cuMulticastAddDevice:", rc)
+for nd in (1, 2):
+    for ht in (0, 1, 8):
+        h = ctypes.c_ulonglong()
+        p = Prop(nd, max(gran.value, 2 << 20), ht, 0)
+        rc = cu.cuMulticastCreate(ctypes.byref(h), ctypes.byref(p))
+        extra = ""
+        if rc == 0:
+            extra = f" addDevice(0) -> {cu.cuMulticastAddDevice(h, 0)}"
+        print(f"cuMulticastCreate(numDevices={nd}, handleTypes={ht}): {rc}{extra}")
