@@ -38,6 +38,21 @@
 #ifndef MUX_DEC_EVICT_FIRST
 #define MUX_DEC_EVICT_FIRST 1
 #endif
+// A/B switch: mbarrier waits of the producers (bit 0) / consumers (bit 1) as sleeping try_waits
+// (suspend-time hint) instead of spins
+#ifndef MUX_DEC_SLEEP
+#define MUX_DEC_SLEEP 0
+#endif
+#if MUX_DEC_SLEEP & 1
+#define DEC_WAIT_P(b, ph) dev::mbar_wait_sleep(b, ph, 2000)
+#else
+#define DEC_WAIT_P(b, ph) dev::mbar_wait(b, ph)
+#endif
+#if MUX_DEC_SLEEP & 2
+#define DEC_WAIT_C(b, ph) dev::mbar_wait_sleep(b, ph, 2000)
+#else
+#define DEC_WAIT_C(b, ph) dev::mbar_wait(b, ph)
+#endif
 
 namespace mux {
 namespace {
@@ -205,7 +220,7 @@ __global__ void __launch_bounds__(DecodeCfg<NT>::kThreads, DecodeCfg<NT>::kCtasP
       const int page = __shfl_sync(0xffffffffu, ids, i & 31);
       const int s = i % STAGES;
       if (lane == 0) {
-        if (i >= STAGES) dev::mbar_wait(&empty[s], ((i / STAGES) - 1) & 1);
+        if (i >= STAGES) DEC_WAIT_P(&empty[s], ((i / STAGES) - 1) & 1);
         dev::mbar_expect_tx(&full[s], L::kStageBytes);
 #if MUX_DEC_EVICT_FIRST
         dev::tma_load_5d_hint(ring + s * L::kStageBytes, map, &full[s], 0, 0, 0, grp * HG, p.page_row0 + page, pol);
@@ -234,7 +249,7 @@ __global__ void __launch_bounds__(DecodeCfg<NT>::kThreads, DecodeCfg<NT>::kCtasP
     int it = 0;
     for (int i = pl; i < n_my; i += kWarpsPerHead, ++it) {
       const int s = i % STAGES;
-      dev::mbar_wait(&kfull[s], (i / STAGES) & 1);
+      DEC_WAIT_C(&kfull[s], (i / STAGES) & 1);
       uint8_t* kbuf = smem + s * L::kStageBytes + hw * L::kHeadBytes;
       uint8_t* vbuf = smem + L::kVOff + s * L::kStageBytes + hw * L::kHeadBytes;
       const int pos0 = (pg0 + i) * kPage;
@@ -322,7 +337,7 @@ __global__ void __launch_bounds__(DecodeCfg<NT>::kThreads, DecodeCfg<NT>::kCtasP
         ph[nt][0] = dev::movmatrix_t(dev::pack_f16(p0, p1));    // tokens 0-7  -> b0
         ph[nt][1] = dev::movmatrix_t(dev::pack_f16(p2, p3));    // tokens 8-15 -> b1
       }
-      dev::mbar_wait(&vfull[s], (i / STAGES) & 1);
+      DEC_WAIT_C(&vfull[s], (i / STAGES) & 1);
       if (valid < kPage) {
         // slots past the sequence end may hold anything (NaN-poisoned in tests): zero this warp's
         // V columns there so P = 0 never meets NaN in the PV MMA; K rows are masked by select.

@@ -203,3 +203,41 @@ def test_run_layer_outproj_and_allreduce_hook(mux, part):
     finally:
         for c in comms:
             c.close()
+
+
+def test_run_layer_allreduce_enqueued_from_c(mux, part):
+    """a7 / §8e: libmux enqueues each layer's NCCL all-reduce of the out-projection itself
+    (mux_side.ar_fn / ar_comm: the ncclAllReduce entry point + a communicator per side), on the
+    side's partition stream, with no Python in the layer loop.  World 1: y is bitwise the
+    standalone out-projection of the side's own attention output."""
+    import torch
+    from paper_2504_14489_b200 import nccl
+    import synth
+    Hq, Hkv, d, hidden = 8, 2, 128, 256
+    pf, dc, pool, g_pf, g_dc = _workload(mux, Hq, Hkv, d)
+    wo_bits = synth.make_wo(802, Shapes(Hq, Hkv, d, 1, hidden=hidden))
+    w_o = mux.mux_outproj_pack_w(torch.from_numpy(wo_bits.view(np.int16)).cuda().view(torch.bfloat16))
+    comms = [nccl.Comm(0, 1), nccl.Comm(0, 1)]
+    try:
+        for split in (-1, 0):
+            ws = torch.empty(max(16, mux.mux_decode_workspace_bytes(3, Hq, d, 2)), dtype=torch.uint8, device="cuda")
+            o_pf = torch.empty((429, Hq, d), dtype=torch.bfloat16, device="cuda")
+            o_dc = torch.empty((3, Hq, d), dtype=torch.bfloat16, device="cuda")
+            y_pf = torch.empty((429, hidden), dtype=torch.bfloat16, device="cuda")
+            y_dc = torch.empty((3, hidden), dtype=torch.bfloat16, device="cuda")
+            # layer 0 holds the workload's K/V (layer 1 of the pool is NaN-poisoned)
+            s_pf = mux.make_side(g_pf["batch"], Hq, g_pf["q"], o_pf, scale=1 / math.sqrt(d), num_layers=1,
+                                 w_o=w_o, y=y_pf, allreduce=comms[1].c_allreduce())
+            s_dc = mux.make_side(g_dc["batch"], Hq, g_dc["q"], o_dc, scale=1 / math.sqrt(d), num_splits=2, ws=ws,
+                                 num_layers=1, w_o=w_o, y=y_dc, allreduce=comms[0].c_allreduce())
+            assert (mux.mux_side_plan(s_pf, pool.desc.num_layers)[:, 1] == 429 * hidden).all()
+            mux.mux_run_layer(part, split, pool, s_pf, s_dc, None)
+            torch.cuda.synchronize()
+            for o, y in ((o_pf, y_pf), (o_dc, y_dc)):
+                y2 = torch.empty_like(y)
+                mux.mux_outproj(o.view(o.shape[0], -1), w_o, y2)
+                torch.cuda.synchronize()
+                assert not torch.isnan(y).any() and torch.equal(y, y2), f"split {split}"
+    finally:
+        for c in comms:
+            c.close()
