@@ -705,6 +705,13 @@ def main():
                       "num_splits": ns})
         return entry
 
+    if world > 1:
+        # every rank must issue the same collectives (a decode layer's all-reduce per D): the candidate
+        # decode-layer counts come from rank 0's isolated timings
+        dl = torch.tensor([e["dc_layers"] for e in sweep], dtype=torch.int64, device="cuda")
+        dist.broadcast(dl, 0)
+        for e, v in zip(sweep, dl.tolist()):
+            e["dc_layers"] = int(v)
     seen = set()
     for e in list(sweep):
         key = (e["split"], e["dc_layers"])
