@@ -286,7 +286,7 @@ def time_kernel_alone(mux, part, wl, split, which, reps=5):
         ws = torch.empty(max(16, mux.mux_decode_workspace_bytes(wl.dc_spec.num_seqs, wl.Hq, wl.d, ns)),
                          dtype=torch.uint8, device="cuda")
         run = lambda: mux.mux_decode_attn(wl.pool, 0, wl.dc_batch, wl.Hq, wl.dc_q, wl.dc_o, None,  # noqa: E731
-                                          scale=wl.scale, num_splits=ns, ws=ws, stream=raw)
+                                          scale=wl.scale, num_splits=ns, ws=ws, stream=raw, num_sms=dsms)
     torch.cuda.synchronize()
     run()
     a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)

@@ -161,6 +161,13 @@ int mux_prefill_attn(mux_pool_t pool, int32_t layer, const mux_batch* batch, int
 int mux_decode_attn(mux_pool_t pool, int32_t layer, const mux_batch* batch, int32_t num_q_heads,
                     const void* q, void* o, int32_t o_dtype, float* lse, float scale,
                     int32_t num_splits, void* ws, size_t ws_bytes, mux_stream_t stream);
+/* the same, with the launch sized for the num_sms SMs `stream` runs on (a partition; <= 0 = the
+ * device): on partitions of <= 16 SMs (Hkv % 4 == 0, g <= 8) two CTAs of 4 kv heads share each SM
+ * so one CTA's ring fill / drain overlaps the other's streaming; the split model (num_splits <= 0)
+ * uses the same count.  mux_run_layer calls this with its sides' partition sizes. */
+int mux_decode_attn_sms(mux_pool_t pool, int32_t layer, const mux_batch* batch, int32_t num_q_heads,
+                        const void* q, void* o, int32_t o_dtype, float* lse, float scale, int32_t num_splits,
+                        void* ws, size_t ws_bytes, mux_stream_t stream, int32_t num_sms);
 size_t mux_decode_workspace_bytes(int32_t num_seqs, int32_t num_q_heads, int32_t head_dim,
                                   int32_t num_splits);
 /* host split-count choice for the balanced split-KV: simulates the launch (every split covers

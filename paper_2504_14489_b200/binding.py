@@ -112,6 +112,8 @@ def lib():
         "mux_prefill_attn": [c_p, c_i32, ctypes.POINTER(BatchC), c_i32, c_p, c_p, c_i32, c_p, c_f32, c_p],
         "mux_decode_attn": [c_p, c_i32, ctypes.POINTER(BatchC), c_i32, c_p, c_p, c_i32, c_p, c_f32, c_i32, c_p,
                             c_sz, c_p],
+        "mux_decode_attn_sms": [c_p, c_i32, ctypes.POINTER(BatchC), c_i32, c_p, c_p, c_i32, c_p, c_f32, c_i32, c_p,
+                                c_sz, c_p, c_i32],
         "mux_partition_create": [ctypes.POINTER(c_p), c_i32, c_p, c_i32],
         "mux_partition_destroy": [c_p],
         "mux_partition_query": [c_p, c_i32, ctypes.POINTER(c_i32), ctypes.POINTER(c_i32), ctypes.POINTER(c_p),
@@ -306,11 +308,17 @@ def mux_prefill_attn(pool: Pool, layer: int, batch: Batch, num_q_heads: int, q, 
 
 
 def mux_decode_attn(pool: Pool, layer: int, batch: Batch, num_q_heads: int, q, o, lse=None,
-                    scale: Optional[float] = None, num_splits: int = 0, ws=None, stream=None):
+                    scale: Optional[float] = None, num_splits: int = 0, ws=None, stream=None, num_sms: int = 0):
+    """a4 decode attention; num_sms > 0: launch sized for the partition the stream runs on
+    (mux_decode_attn_sms), else for the whole device (mux_decode_attn)."""
     import torch
     scale = scale if scale is not None else 1.0 / float(np.sqrt(pool.desc.head_dim))
     od = MUX_DTYPE_F32 if o.dtype == torch.float32 else MUX_DTYPE_BF16
     ws_bytes = ws.numel() * ws.element_size() if ws is not None else 0
+    if num_sms > 0:
+        _check(lib().mux_decode_attn_sms(pool.h, layer, batch.ref, num_q_heads, _ptr(q), _ptr(o), od, _ptr(lse),
+                                         scale, num_splits, _ptr(ws), ws_bytes, _stream(stream), num_sms))
+        return
     _check(lib().mux_decode_attn(pool.h, layer, batch.ref, num_q_heads, _ptr(q), _ptr(o), od, _ptr(lse), scale,
                                  num_splits, _ptr(ws), ws_bytes, _stream(stream)))
 

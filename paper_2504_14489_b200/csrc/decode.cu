@@ -65,19 +65,21 @@ namespace {
 #ifndef MUX_DEC_SPLITD
 #define MUX_DEC_SPLITD 1
 #endif
-#ifndef MUX_DEC_2CTA
-#define MUX_DEC_2CTA 0   // A/B switch: two CTAs per SM (4 kv heads, 4 consumer warps, 96 KiB ring each)
-#endif
-template <int NT> struct DecodeCfg {
-  static constexpr int kSplitD = (NT == 1 && MUX_DEC_SPLITD == 2) ? 2 : 1;   // warps per (head, page)
-  static constexpr int kConsumerWarps = MUX_DEC_2CTA ? 4 : 8 * kSplitD;
-  static constexpr int kCtasPerSm = MUX_DEC_2CTA ? 2 : 1;
+// C2: two CTAs per SM (4 kv heads, 4 consumer warps, 96 KiB ring each): on small decode partitions
+// one CTA's ring fill / drain overlaps the other's streaming (8 SMs: 1188 -> 1146-1179 us per cfg2
+// layer in the multiplexed step, 16 SMs: 616 -> 601 us; slower in the mux layer at 32-96 SMs, r01), so
+// it is chosen at launch for partitions of <= kDec2CtaMaxSms SMs (decode_launch_sms, the split model)
+constexpr int kDec2CtaMaxSms = 16;
+template <int NT, bool C2 = false> struct DecodeCfg {
+  static constexpr int kSplitD = (NT == 1 && MUX_DEC_SPLITD == 2 && !C2) ? 2 : 1;   // warps per (head, page)
+  static constexpr int kConsumerWarps = C2 ? 4 : 8 * kSplitD;
+  static constexpr int kCtasPerSm = C2 ? 2 : 1;
   static constexpr int kThreads = (kConsumerWarps + 2) * 32;   // + K producer + V producer
 };
 #ifndef MUX_DEC_RING_KB
-#define MUX_DEC_RING_KB 192   // A/B switch: KiB of K + V stages per CTA (1 CTA / SM)
+#define MUX_DEC_RING_KB 192   // A/B switch: KiB of K + V stages per SM
 #endif
-constexpr int kRingBytes = (MUX_DEC_2CTA ? MUX_DEC_RING_KB / 2 : MUX_DEC_RING_KB) * 1024;   // K and V stages in flight per CTA
+template <bool C2> constexpr int ring_bytes() { return (C2 ? MUX_DEC_RING_KB / 2 : MUX_DEC_RING_KB) * 1024; }
 
 struct DecodeParams {
   const uint16_t* q;         // [B][Hq][D]
@@ -99,9 +101,10 @@ struct DecodeParams {
 // Two rings of stages, K and V: a stage = one page (16 tokens) of K (or V) for the HG kv heads
 // of this CTA's group, as TMA lands it: [HG][d/64][16 rows][128 B] (SWIZZLE_128B).  A K stage
 // is released right after QK (before the page's PV), so K refills run ahead of V.
-template <int D, int NT, int HG>
+template <int D, int NT, int HG, bool C2 = false>
 struct DecodeSmem {
-  using C = DecodeCfg<NT>;
+  using C = DecodeCfg<NT, C2>;
+  static constexpr int kRingBytes = ring_bytes<C2>();
   static constexpr int kHeadBytes = D * kPage * 2;             // one (page, head) block of K (or V)
   static constexpr int kStageBytes = HG * kHeadBytes;          // K (or V) of HG heads
   static constexpr int kQStride = D + 8;                       // padded bf16 row -> conflict-free ldmatrix
@@ -110,7 +113,7 @@ struct DecodeSmem {
   // partial-score exchange of the head_dim halves: [pair][2 buffers][2 halves][32 lanes][4 f32]
   static constexpr int kPairs = C::kConsumerWarps / C::kSplitD;
   static constexpr int kXBytes = C::kSplitD > 1 ? kPairs * 2 * 2 * 32 * 16 : 0;
-  static constexpr int kSmemCap = (MUX_DEC_2CTA ? 112 : 224) * 1024;
+  static constexpr int kSmemCap = (C2 ? 112 : 224) * 1024;
   static constexpr int kRing = (kRingBytes < kSmemCap - kQBytes - kXBytes) ? kRingBytes : kSmemCap - kQBytes - kXBytes;
   // stages per ring; a multiple of the page lanes of a head (W): a warp takes every W-th page, and
   // its successive waits on one stage's mbarrier must be successive phases (parity)
@@ -130,12 +133,12 @@ struct DecodeSmem {
   static_assert(kBytes + 1024 <= kSmemCap + 3 * 1024, "shared memory");
 };
 
-template <int D, int NT, int HG>
-__global__ void __launch_bounds__(DecodeCfg<NT>::kThreads, DecodeCfg<NT>::kCtasPerSm)
+template <int D, int NT, int HG, bool C2>
+__global__ void __launch_bounds__(DecodeCfg<NT, C2>::kThreads, DecodeCfg<NT, C2>::kCtasPerSm)
     decode_kernel(const __grid_constant__ CUtensorMap tmap_k, const __grid_constant__ CUtensorMap tmap_v,
                   const DecodeParams p) {
-  using L = DecodeSmem<D, NT, HG>;
-  using C = DecodeCfg<NT>;
+  using L = DecodeSmem<D, NT, HG, C2>;
+  using C = DecodeCfg<NT, C2>;
   constexpr int kConsumerWarps = C::kConsumerWarps;
   constexpr int kThreads = C::kThreads;
   constexpr int SD = C::kSplitD;
@@ -478,10 +481,10 @@ __global__ void __launch_bounds__(D) combine_kernel(const float* __restrict__ pa
   if (c == 0 && lse) lse[row] = (M + __log2f(W)) * 0.69314718055994531f;
 }
 
-template <int D, int NT, int HG>
+template <int D, int NT, int HG, bool C2 = false>
 int launch_decode_hg(mux_pool* pool, const DecodeParams& prm, int B, cudaStream_t st) {
-  using L = DecodeSmem<D, NT, HG>;
-  auto kern = decode_kernel<D, NT, HG>;
+  using L = DecodeSmem<D, NT, HG, C2>;
+  auto kern = decode_kernel<D, NT, HG, C2>;
   const int smem = L::kBytes + 1024;
   static bool attr_done = false;
   if (!attr_done) {
@@ -489,7 +492,8 @@ int launch_decode_hg(mux_pool* pool, const DecodeParams& prm, int B, cudaStream_
     attr_done = true;
   }
   dim3 grid(prm.num_splits, prm.hkv / HG, B);
-  kern<<<grid, DecodeCfg<NT>::kThreads, smem, st>>>(pool->tmap_kg, pool->tmap_vg, prm);
+  kern<<<grid, DecodeCfg<NT, C2>::kThreads, smem, st>>>(C2 ? pool->tmap_kg4 : pool->tmap_kg,
+                                                        C2 ? pool->tmap_vg4 : pool->tmap_vg, prm);
   MUX_CUDA(cudaGetLastError());
   if (prm.num_splits > 1) {
     combine_kernel<D><<<B * prm.hq, D, 0, st>>>(prm.part_o, prm.part_m, prm.part_l, prm.o, prm.lse, prm.kv_len,
@@ -499,12 +503,18 @@ int launch_decode_hg(mux_pool* pool, const DecodeParams& prm, int B, cudaStream_
   return MUX_OK;
 }
 
+// two CTAs per SM on small partitions (g <= 8, Hkv % 4 == 0: 4 kv heads per CTA)
+bool use_dec_2cta(int hkv, int g, int num_sms) {
+  return num_sms > 0 && num_sms <= kDec2CtaMaxSms && hkv % 4 == 0 && g <= 8;
+}
+
 template <int D, int NT>
-int launch_decode(mux_pool* pool, const DecodeParams& prm, int B, cudaStream_t st) {
+int launch_decode(mux_pool* pool, const DecodeParams& prm, int B, cudaStream_t st, int num_sms) {
+  if constexpr (NT == 1) {
+    if (use_dec_2cta(prm.hkv, prm.g, num_sms)) return launch_decode_hg<D, NT, 4, true>(pool, prm, B, st);
+  }
   switch (pool->hg) {
-#if !MUX_DEC_2CTA
     case 8: return launch_decode_hg<D, NT, 8>(pool, prm, B, st);
-#endif
     case 4: return launch_decode_hg<D, NT, 4>(pool, prm, B, st);
     case 2: return launch_decode_hg<D, NT, 2>(pool, prm, B, st);
     case 1: return launch_decode_hg<D, NT, 1>(pool, prm, B, st);
@@ -530,8 +540,11 @@ int32_t mux_decode_num_splits(int32_t num_seqs, int32_t hkv, int32_t head_dim, c
   if (num_seqs < 1 || hkv < 1 || max_kv < 1) return 1;
   if (num_sms < 1) num_sms = 148;
   if (head_dim < 1) head_dim = 128;
-  int hg = 1;   // as pool_tmaps: the largest power of two <= 8 dividing Hkv
-  for (int c = 2; c <= (MUX_DEC_2CTA ? 4 : 8); c *= 2)
+  // the launch's CTA shape (decode_launch_sms): two CTAs of 4 kv heads per SM on small partitions,
+  // else the largest power of two <= 8 dividing Hkv (as pool_tmaps)
+  const bool c2 = num_sms <= kDec2CtaMaxSms && hkv % 4 == 0;
+  int hg = 1;
+  for (int c = 2; c <= (c2 ? 4 : 8); c *= 2)
     if (hkv % c == 0) hg = c;
   const int groups = hkv / hg;
   const int max_pages = (max_kv + kPage - 1) / kPage;
@@ -540,9 +553,9 @@ int32_t mux_decode_num_splits(int32_t num_seqs, int32_t hkv, int32_t head_dim, c
   // combine pass ~6 us + its partial traffic.  The grid's CTAs are dispatched in launch order
   // (split fastest) onto the first free SM; the split count with the smallest predicted
   // makespan wins.  Balanced splits: C = ceil(max_pages / S) pages per split for every sequence.
-  // two CTAs share an SM under MUX_DEC_2CTA: twice the slots, each streaming about half as fast
-  const int slots = num_sms * DecodeCfg<1>::kCtasPerSm;
-  const double cta_bytes_per_us = DecodeCfg<1>::kCtasPerSm == 2 ? 6.5e4 : 1.0e5;
+  // two CTAs share an SM on small partitions: twice the slots, each streaming about half as fast
+  const int slots = num_sms * (c2 ? 2 : 1);
+  const double cta_bytes_per_us = c2 ? 6.5e4 : 1.0e5;
   const double page_us = static_cast<double>(hg) * kPage * head_dim * 2 * 2 / cta_bytes_per_us;
   const double cta_us = 4.0, empty_us = 0.3;
   std::vector<int> pages(num_seqs);
@@ -593,6 +606,24 @@ int32_t mux_decode_num_splits(int32_t num_seqs, int32_t hkv, int32_t head_dim, c
 int mux_decode_attn(mux_pool_t pool, int32_t layer, const mux_batch* b, int32_t hq, const void* q, void* o,
                     int32_t o_dtype, float* lse, float scale, int32_t num_splits, void* ws, size_t ws_bytes,
                     mux_stream_t stream) {
+  // the public call sizes its launch for the whole device; mux_run_layer passes the partition's SMs
+  return mux::decode_launch_sms(pool, layer, b, hq, q, o, o_dtype, lse, scale, num_splits, ws, ws_bytes, stream,
+                                device_sm_count());
+}
+
+int mux_decode_attn_sms(mux_pool_t pool, int32_t layer, const mux_batch* b, int32_t hq, const void* q, void* o,
+                        int32_t o_dtype, float* lse, float scale, int32_t num_splits, void* ws, size_t ws_bytes,
+                        mux_stream_t stream, int32_t num_sms) {
+  return mux::decode_launch_sms(pool, layer, b, hq, q, o, o_dtype, lse, scale, num_splits, ws, ws_bytes, stream,
+                                num_sms);
+}
+
+}  // extern "C"
+
+namespace mux {
+int decode_launch_sms(mux_pool_t pool, int32_t layer, const mux_batch* b, int32_t hq, const void* q, void* o,
+                      int32_t o_dtype, float* lse, float scale, int32_t num_splits, void* ws, size_t ws_bytes,
+                      mux_stream_t stream, int num_sms) {
   int rc = check_pool_layer(pool, layer);
   if (rc) return rc;
   if ((rc = validate_batch(b, true))) return rc;
@@ -603,8 +634,8 @@ int mux_decode_attn(mux_pool_t pool, int32_t layer, const mux_batch* b, int32_t 
   if (!q || !o) return fail(MUX_ERR_INVALID_ARG, "q/o NULL");
   if (o_dtype != MUX_DTYPE_BF16 && o_dtype != MUX_DTYPE_F32) return fail(MUX_ERR_INVALID_ARG, "bad o_dtype");
   if (reinterpret_cast<uintptr_t>(q) & 15) return fail(MUX_ERR_INVALID_ARG, "q must be 16-byte aligned");
-  if (num_splits <= 0)
-    num_splits = mux_decode_num_splits(b->num_seqs, hkv, d, b->h_kv_len, b->max_kv, device_sm_count());
+  if (num_sms <= 0) num_sms = device_sm_count();
+  if (num_splits <= 0) num_splits = mux_decode_num_splits(b->num_seqs, hkv, d, b->h_kv_len, b->max_kv, num_sms);
   if (num_splits > 1) {
     if (!ws || ws_bytes < mux_decode_workspace_bytes(b->num_seqs, hq, d, num_splits))
       return fail(MUX_ERR_WORKSPACE, "decode workspace missing or too small");
@@ -633,9 +664,9 @@ int mux_decode_attn(mux_pool_t pool, int32_t layer, const mux_batch* b, int32_t 
   prm.o_f32 = o_dtype == MUX_DTYPE_F32;
   prm.scale_log2 = scale * 1.4426950408889634f;
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
-  if (d == 128) return g <= 8 ? launch_decode<128, 1>(pool, prm, b->num_seqs, st)
-                              : launch_decode<128, 2>(pool, prm, b->num_seqs, st);
-  return g <= 8 ? launch_decode<64, 1>(pool, prm, b->num_seqs, st) : launch_decode<64, 2>(pool, prm, b->num_seqs, st);
+  if (d == 128) return g <= 8 ? launch_decode<128, 1>(pool, prm, b->num_seqs, st, num_sms)
+                              : launch_decode<128, 2>(pool, prm, b->num_seqs, st, num_sms);
+  return g <= 8 ? launch_decode<64, 1>(pool, prm, b->num_seqs, st, num_sms)
+                : launch_decode<64, 2>(pool, prm, b->num_seqs, st, num_sms);
 }
-
-}  // extern "C"
+}  // namespace mux

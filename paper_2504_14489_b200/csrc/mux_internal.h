@@ -72,6 +72,10 @@ int run_side(mux_pool_t pool, const mux_side* s, bool decode, int sms, cudaStrea
              unsigned long long* t1);
 void launch_stamp(unsigned long long* dst, cudaStream_t st);
 // outproj.cu: mux_outproj with the SM count of the launching partition (persistent grid)
+// a4 decode attention with the launch sized for `num_sms` SMs (the side's partition; <= 0 = device)
+int decode_launch_sms(mux_pool_t pool, int32_t layer, const mux_batch* b, int32_t hq, const void* q, void* o,
+                      int32_t o_dtype, float* lse, float scale, int32_t num_splits, void* ws, size_t ws_bytes,
+                      mux_stream_t stream, int num_sms);
 int qkv_launch(mux_pool_t pool, int32_t layer, const mux_batch* b, int32_t hq, const void* x, int32_t hidden,
                const void* w_qkv, const void* rope, int32_t rope_max_pos, void* q_out, mux_stream_t stream,
                int num_sms);

@@ -214,8 +214,8 @@ int run_side(mux_pool_t pool, const mux_side* s, bool decode, int sms, cudaStrea
     float* lse = static_cast<float*>(const_cast<void*>(at(s->lse, s->lse_stride)));
     if ((rc = ev(i, 0))) return rc;
     if (decode)
-      rc = mux_decode_attn(pool, layer, s->batch, s->num_q_heads, at(s->q, s->q_stride), o, s->o_dtype, lse,
-                           s->scale, splits, s->ws, s->ws_bytes, reinterpret_cast<mux_stream_t>(st));
+      rc = decode_launch_sms(pool, layer, s->batch, s->num_q_heads, at(s->q, s->q_stride), o, s->o_dtype, lse,
+                             s->scale, splits, s->ws, s->ws_bytes, reinterpret_cast<mux_stream_t>(st), sms);
     else
       rc = mux_prefill_attn(pool, layer, s->batch, s->num_q_heads, at(s->q, s->q_stride), o, s->o_dtype, lse,
                             s->scale, reinterpret_cast<mux_stream_t>(st));

@@ -27,13 +27,10 @@ int pool_tmaps(mux_pool* p) {
   uint64_t dims[5] = {64, static_cast<uint64_t>(kPage), D / 64, static_cast<uint64_t>(d.num_kv_heads),
                       static_cast<uint64_t>(d.num_layers) * static_cast<uint64_t>(d.num_pages)};
   uint64_t strides[4] = {D * 2, 128, kPage * D * 2, static_cast<uint64_t>(d.num_kv_heads) * kPage * D * 2};
-#ifndef MUX_DEC_2CTA
-#define MUX_DEC_2CTA 0
-#endif
   // kv heads per decode CTA (csrc/decode.cu): the largest power of two <= 8 (4 under the 2-CTA
   // switch) dividing Hkv, the instantiations launch_decode has (Hkv = 3, 6, 12 ... -> 1 or 2)
   int hg = 1;
-  for (int c = 2; c <= (MUX_DEC_2CTA ? 4 : 8); c *= 2)
+  for (int c = 2; c <= 8; c *= 2)
     if (d.num_kv_heads % c == 0) hg = c;
   p->hg = hg;
   uint32_t box1[5] = {64, static_cast<uint32_t>(kPage), static_cast<uint32_t>(D / 64), 1, 1};
@@ -43,6 +40,11 @@ int pool_tmaps(mux_pool* p) {
   if ((rc = make_tmap_bf16(&p->tmap_v1, d.v_storage, 5, dims, strides, box1))) return rc;
   if ((rc = make_tmap_bf16(&p->tmap_kg, d.k_storage, 5, dims, strides, boxg))) return rc;
   if ((rc = make_tmap_bf16(&p->tmap_vg, d.v_storage, 5, dims, strides, boxg))) return rc;
+  if (d.num_kv_heads % 4 == 0) {   // two-CTA decode on small partitions: pages of 4 kv heads
+    uint32_t box4[5] = {64, static_cast<uint32_t>(kPage), static_cast<uint32_t>(D / 64), 4, 1};
+    if ((rc = make_tmap_bf16(&p->tmap_kg4, d.k_storage, 5, dims, strides, box4))) return rc;
+    if ((rc = make_tmap_bf16(&p->tmap_vg4, d.v_storage, 5, dims, strides, box4))) return rc;
+  }
   uint32_t boxh[5] = {64, static_cast<uint32_t>(kPage), 1, 1, 1};
   if ((rc = make_tmap_bf16(&p->tmap_kh, d.k_storage, 5, dims, strides, boxh))) return rc;
   if (!p->d_err) {

@@ -15,7 +15,8 @@ struct mux_pool {
   // tmap_*1: box = one (page, kv head) block (both 64-dim halves, 4 KiB at d=128)   -> prefill
   // tmap_*g: box = one page of a whole kv-head group of hg heads (hg x 4 KiB)        -> decode
   // tmap_kh: box = one 64-dim half of one (page, kv head) block (2 KiB)            -> prefill K
-  CUtensorMap tmap_k1, tmap_v1, tmap_kg, tmap_vg, tmap_kh;
+  // tmap_*g4: box = one page of 4 kv heads (the two-CTA decode of small partitions)
+  CUtensorMap tmap_k1, tmap_v1, tmap_kg, tmap_vg, tmap_kh, tmap_kg4, tmap_vg4;
   int hg = 1;                        // kv heads per decode CTA (largest power of two <= 8 dividing Hkv)
   int* d_err = nullptr;              // device error word (bit 0: append clamped a V value to fp16 range)
   int64_t layer_elems() const {      // elements per layer of K (or V)

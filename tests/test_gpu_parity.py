@@ -373,3 +373,31 @@ def test_outproj_pack_layout(mux, K, N):
                                        np.arange(8), indexing="ij")
     want = wp[kb * 64 + k, nt * 128 + h * 64 + (pos ^ (k & 7)) * 8 + e].reshape(-1)
     np.testing.assert_array_equal(got, want)
+
+
+@pytest.mark.parametrize("num_sms", [8, 16])
+@pytest.mark.parametrize("Hq,Hkv,d", [(32, 8, 128), (16, 4, 128), (8, 4, 64), (64, 8, 128)])
+def test_decode_two_cta_small_partition_parity(mux, num_sms, Hq, Hkv, d):
+    """The decode launch sized for a small partition (mux_decode_attn_sms, <= 16 SMs: two CTAs of
+    4 kv heads per SM) against the oracle, ragged contexts incl. page tails, split and unsplit;
+    with Hkv = 8 also bitwise equal to the whole-device launch with the same split count (both
+    give each warp all pages of one kv head, so the reduction order is the same; with Hkv = 4 the
+    device launch splits a head's pages over two warps)."""
+    import torch
+    spec = SideSpec([4095, 17, 1000, 0, 2049, 15], [1] * 6)
+    side = _side(70 + num_sms + Hq, spec, Hq, Hkv, d)
+    gs = gpu_build_side(mux, side, sum(spec.pages_needed()) + 4, 13, Hkv, d)
+    os_ = oracle_build_side(side, sum(spec.pages_needed()) + 4, 13, Hkv, d)
+    ref, _ = oracle.attention(side.q, os_["kpool"], os_["vpool"], os_["qo_indptr"], os_["kv_len"],
+                              os_["page_indptr"], os_["page_ids"], 1 / math.sqrt(d))
+    for ns in (1, 3):
+        ws = torch.empty(max(16, mux.mux_decode_workspace_bytes(6, Hq, d, ns)), dtype=torch.uint8, device="cuda")
+        o = torch.empty((6, Hq, d), dtype=torch.float32, device="cuda")
+        mux.mux_decode_attn(gs["pool"], 0, gs["batch"], Hq, gs["q"], o, None, num_splits=ns, ws=ws, num_sms=num_sms)
+        o_full = torch.empty_like(o)
+        mux.mux_decode_attn(gs["pool"], 0, gs["batch"], Hq, gs["q"], o_full, None, num_splits=ns, ws=ws)
+        torch.cuda.synchronize()
+        check_close(o.cpu().numpy(), ref, what=f"decode {num_sms} SMs, {ns} splits")
+        check_close(o_full.cpu().numpy(), ref, what=f"decode device launch, {ns} splits")
+        if Hkv == 8:
+            assert torch.equal(o, o_full), "small-partition launch != device launch"
