@@ -722,8 +722,11 @@ def main():
         measure_mux(e)
     # the paper's serving objective is goodput under SLOs: the split must keep a decode token's
     # time between tokens (an iteration = N_T layers = N_T / D steps) within the TBT SLO
-    ok = [e for e in sweep if e["tbt_ms"] <= args.tbt_slo_ms]
-    best = max(ok or sweep, key=lambda e: e["tok_s"])
+    ok = [e for e in sweep if e["tbt_ms"] <= args.tbt_slo_ms] or sweep
+    best = max(ok, key=lambda e: e["tok_s"])
+    # bubble-less: among candidates within 1 % of the best rate, the most balanced sides
+    near = [e for e in ok if e["tok_s"] >= 0.99 * best["tok_s"]]
+    best = min(near, key=lambda e: abs(e["dec_side_ms"] - e["pf_side_ms"]) / max(e["dec_side_ms"], e["pf_side_ms"]))
     if world > 1:  # every rank must run the same split: rank 0 decides
         t = torch.tensor([sweep.index(best)], device="cuda")
         dist.broadcast(t, 0)
