@@ -678,7 +678,7 @@ def main():
         t_pf = time_side(mux, part, i, wl, "pf", NT)          # the whole prefill (N_T layers)
         r = t_pf / (t_dc / NT)                                 # decode layers per prefill window
         # contention slows the decode side more than the prefill side: candidates below r too
-        for f in (0.8, 0.9, 1.0):
+        for f in (0.7, 0.8, 0.9, 1.0):
             sweep.append({"split": i, "dec_sms": dsms, "pf_sms": psms, "t_dc_iso_ms": t_dc * 1e3,
                           "t_pf_iso_ms": t_pf * 1e3, "dc_layers": max(1, int(round(r * f)))})
 
