@@ -1,0 +1,167 @@
+// Developer microbenchmark: does a running tcgen05.mma stream (the prefill's QK SS / PV TS shapes)
+// slow the softmax exp mix (ffma2, 2 x MUFU.EX2, add.f32x2, f16x2 pack per pair) of other warps?
+// One CTA per SM: warp 0 = MMA issuer (mode-dependent), warps 1..8 = exp warps (2 per SMSP).
+//   nvcc -gencode arch=compute_100a,code=sm_100a -O3 -std=c++17 -I include scripts/ubench_mufu_mma.cu -o scripts/ubench_mufu_mma
+#include <cstdio>
+#include "../paper_2504_14489_b200/csrc/mux_internal.h"
+using namespace mux;
+
+__device__ __forceinline__ float exp_mix(uint32_t (&s)[64], float sl2, float neg_m) {
+  const uint64_t S2 = dev::f2pack(sl2, sl2), OF = dev::f2pack(neg_m, neg_m);
+  uint64_t acc = dev::f2pack(0.f, 0.f);
+#pragma unroll
+  for (int i = 0; i < 32; ++i) {
+    float a, b;
+    dev::f2unpack(dev::ffma2(dev::f2pack(__uint_as_float(s[2 * i]), __uint_as_float(s[2 * i + 1])), S2, OF), a, b);
+    const float e0 = dev::ex2(a), e1 = dev::ex2(b);
+    acc = dev::fadd2(acc, dev::f2pack(e0, e1));
+    const uint32_t pk = dev::pack_f16(e0, e1);
+    s[2 * i] ^= pk & 1u;
+    s[2 * i + 1] ^= (pk >> 16) & 1u;
+  }
+  float a0, a1;
+  dev::f2unpack(acc, a0, a1);
+  return a0 + a1;
+}
+
+__global__ void __launch_bounds__(544, 1) kern(long long* out, int iters, int mode) {
+  extern __shared__ __align__(1024) uint8_t sm[];
+  __shared__ uint64_t bar;
+  __shared__ uint32_t slot;
+  __shared__ volatile int done;
+  __shared__ uint64_t never;
+  uint8_t* s = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(sm) + 1023) & ~uintptr_t(1023));
+  const int warp = threadIdx.x >> 5;
+  if (threadIdx.x == 0) { dev::mbar_init(&bar, 1); dev::mbar_init(&never, 1); dev::fence_mbar_init(); done = 0; }
+  if (warp == 0) dev::tmem_alloc(&slot, 512);
+  for (int i = threadIdx.x; i < 96 * 1024 / 16; i += blockDim.x) reinterpret_cast<uint4*>(s)[i] = make_uint4(0, 0, 0, 0);
+  dev::fence_proxy_async_smem();
+  dev::tc_fence_before();
+  __syncthreads();
+  dev::tc_fence_after();
+  const uint32_t tm = slot;
+  if (warp == 0) {
+    if (threadIdx.x == 0 && mode > 0) {
+      const uint64_t da = dev::umma_desc_sw128(dev::smem_u32(s), 16, 1024);
+      const uint64_t db = dev::umma_desc_sw128(dev::smem_u32(s + 32768), 16, 1024);
+      const uint64_t dv = dev::umma_desc_sw128(dev::smem_u32(s + 65536), 2048, 1024);
+      constexpr uint32_t i128 = dev::umma_idesc_bf16(128, 128, 0, 0);
+      constexpr uint32_t ipv = dev::umma_idesc_f16(128, 128, 0, 1);
+      int r = 0;
+      while (!done) {
+        if (mode == 1 || mode == 2)
+#pragma unroll
+          for (int kk = 0; kk < 8; ++kk) dev::umma_ss(tm, da + ((kk * 32) >> 4), db + ((kk * 32) >> 4), i128, kk > 0);
+        if (mode == 1 || mode == 3)
+#pragma unroll
+          for (int pp = 0; pp < 8; ++pp)
+            dev::umma_ts(tm + 256, tm + 128 + (pp % 4) * 8, dv + (((pp % 4) * 4096) >> 4), ipv, 1u);
+        // keep at most ~2 patterns in flight
+        dev::umma_commit(&bar);
+        dev::mbar_wait(&bar, r & 1);
+        ++r;
+      }
+      if (blockIdx.x == 0) out[2] = r;
+    }
+  } else if (warp >= 9) {
+    // co-running warps (2 per SMSP): 4 = TMEM load of 64 columns + row max, 5 = sleeping mbarrier wait,
+    // 6 = the same exp mix, other modes = exit
+    const uint32_t lane_off = static_cast<uint32_t>((warp & 3) * 32) << 16;
+    float acc = 0.f;
+    if (mode == 4) {
+      while (!done) {
+        uint32_t r[64];
+        dev::tmem_ld32(lane_off + (warp & 1) * 64, *reinterpret_cast<uint32_t(*)[32]>(&r[0]));
+        dev::tmem_ld32(lane_off + (warp & 1) * 64 + 32, *reinterpret_cast<uint32_t(*)[32]>(&r[32]));
+        dev::tmem_wait_ld();
+        float m = -1e30f;
+#pragma unroll
+        for (int i = 0; i < 64; ++i) m = fmaxf(m, __uint_as_float(r[i]));
+        acc += m;
+      }
+    } else if (mode == 7 || mode == 10) {   // pure TMEM loads (10: one 2x32-column load per ~1500 cycles)
+      while (!done) {
+        uint32_t r[64];
+        dev::tmem_ld32(lane_off + (warp & 1) * 64, *reinterpret_cast<uint32_t(*)[32]>(&r[0]));
+        dev::tmem_ld32(lane_off + (warp & 1) * 64 + 32, *reinterpret_cast<uint32_t(*)[32]>(&r[32]));
+        dev::tmem_wait_ld();
+        acc += __uint_as_float(r[0] ^ r[63]);
+        if (mode == 10) {
+          const long long t = clock64();
+          while (clock64() - t < 1500) __nanosleep(100);
+        }
+      }
+    } else if (mode == 8) {   // row max over registers only
+      uint32_t r[64];
+#pragma unroll
+      for (int i = 0; i < 64; ++i) r[i] = __float_as_uint((threadIdx.x + i) * -1e-3f);
+      while (!done) {
+        float m = -1e30f;
+#pragma unroll
+        for (int i = 0; i < 64; ++i) m = fmaxf(m, __uint_as_float(r[i]));
+        acc += m;
+        r[threadIdx.x & 63] ^= 1u;
+      }
+    } else if (mode == 9) {   // TMEM stores of 32 columns (the P store)
+      uint32_t r[32];
+#pragma unroll
+      for (int i = 0; i < 32; ++i) r[i] = threadIdx.x + i;
+      while (!done) {
+        dev::tmem_st16(lane_off + 128 + (warp & 1) * 32, &r[0]);
+        dev::tmem_st16(lane_off + 128 + (warp & 1) * 32 + 16, &r[16]);
+        dev::tmem_wait_st();
+        r[0] += 1;
+      }
+    } else if (mode == 5) {
+      dev::mbar_wait_sleep(&never, 0);
+    } else if (mode == 6) {
+      uint32_t v[64];
+#pragma unroll
+      for (int i = 0; i < 64; ++i) v[i] = __float_as_uint((threadIdx.x + i) * -1e-3f);
+      while (!done) acc += exp_mix(v, 1.4426950f, -0.5f);
+    }
+    if (acc == 12345.f) out[3] = 1;
+  } else {
+    uint32_t v[64];
+#pragma unroll
+    for (int i = 0; i < 64; ++i) v[i] = __float_as_uint((threadIdx.x + i) * -1e-3f);
+    float acc = 0.f;
+    __syncwarp();
+    long long t0 = clock64();
+    for (int it = 0; it < iters; ++it) acc += exp_mix(v, 1.4426950f, -0.5f);
+    long long t1 = clock64();
+    if (acc == 12345.f) out[3] = 1;
+    if (blockIdx.x == 0 && warp == 1 && (threadIdx.x & 31) == 0) out[0] = t1 - t0;
+    asm volatile("bar.sync 1, 256;");
+    if (warp == 1 && (threadIdx.x & 31) == 0) {
+      done = 1;
+      if (mode == 5) dev::mbar_arrive(&never);
+    }
+  }
+  dev::tc_fence_before();
+  __syncthreads();
+  if (warp == 0) { dev::tc_fence_after(); dev::tmem_dealloc(tm, 512); }
+}
+
+int main() {
+  long long* d;
+  cudaMalloc(&d, 64);
+  long long h[4];
+  cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 100 * 1024);
+  const char* names[] = {"exp warps alone", "+ MMA QK(SS)+PV(TS)", "+ MMA QK(SS) only", "+ MMA PV(TS) only",
+                         "+ 2 warps/SMSP LDTM+max", "+ 2 warps/SMSP mbar sleep", "+ 2 warps/SMSP exp mix",
+                         "+ 2 warps/SMSP LDTM only", "+ 2 warps/SMSP FMNMX only", "+ 2 warps/SMSP STTM only",
+                         "+ LDTM every ~1500 cyc"};
+  const int iters = 200;
+  for (int rep = 0; rep < 2; ++rep)
+    for (int mode = 0; mode < 11; ++mode) {
+      cudaMemset(d, 0, 64);
+      kern<<<148, 544, 100 * 1024>>>(d, iters, mode);
+      cudaError_t e = cudaDeviceSynchronize();
+      cudaMemcpy(h, d, 32, cudaMemcpyDeviceToHost);
+      // per iteration: 2 warps per SMSP x 64 ex2 -> MUFU floor 2 * 64 * 8 = 1024 cycles
+      printf("%-24s %s: %.0f cycles per 64-element iteration (2 warps/SMSP; MUFU floor 1024), mma patterns %lld\n",
+             names[mode], cudaGetErrorString(e), double(h[0]) / iters, h[2]);
+    }
+  return 0;
+}
