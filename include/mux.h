@@ -312,6 +312,47 @@ int mux_outproj_sms(const void* x, const void* w_packed, void* y, int32_t y_dtyp
                     int32_t N, mux_stream_t stream, int32_t num_sms);
 
 /* ------------------------------------------------------------------------------------
+ * f4 (fused communication): the out-projection GEMM and the all-reduce of
+ * its partial sums in ONE kernel over peer memory.  PAPER: Llama-70B runs with tensor
+ * parallelism of degree 8 over NVLink; per layer the G KV-head shards'
+ * partials O_g . W_o,g are summed (R23).  Replaces a7's mux_outproj + NCCL all-reduce.
+ *
+ * Rank r computes Y_r = X_r . W_r (X [T][K] bf16 row-major, W PACKED by mux_outproj_pack_w,
+ * fp32 accumulation; 256 x 256 tiles on CTA pairs).  Tile t is owned by rank t mod G: the
+ * epilogue stores each partial tile as bf16 (the wire type of R23) into the OWNER's staging
+ * slot and raises a counter there (release, system scope); each rank sums the G partials of its
+ * tiles in rank order 0..G-1 in fp32 (identical bits on every rank, run to run), rounds to bf16
+ * and stores the tile into EVERY rank's Y [T][N] bf16 (all-gather), counting completions on each
+ * rank; the kernel returns once this rank's Y is complete.  Traffic per rank equals a ring
+ * all-reduce's (2 (G-1)/G of Y), but it leaves the GPU tile by tile during the GEMM.
+ *
+ * peers: world G (1..MUX_AR_MAX_WORLD), this rank, epoch (launch counter shared by all ranks:
+ * 1 on the first call with a workspace, +1 per call; counters are never reset) and, per rank r,
+ * its staging workspace (mux_outproj_ar_ws_bytes(T, N, G) bytes, zero-filled ONCE before the
+ * first call) and its Y, as addresses valid in THIS process (peers' allocations mapped by CUDA
+ * IPC or VMM; rank == r: local).  Every rank calls with the same T, K, N, world and epoch.
+ * num_sms: SMs the launch may use (<= 0: the device); one CTA per SM, so all of a rank's CTAs are
+ * resident and the cross-rank waits cannot deadlock.  Requirements: T > 128, K and N multiples of
+ * 8, 16-byte aligned buffers.  Errors: MUX_ERR_INVALID_ARG / MUX_ERR_UNSUPPORTED / MUX_ERR_CUDA. */
+#define MUX_AR_MAX_WORLD 8
+typedef struct mux_ar_peers {
+  int32_t world;
+  int32_t rank;
+  uint32_t epoch;
+  void* stage[MUX_AR_MAX_WORLD];
+  void* y[MUX_AR_MAX_WORLD];
+} mux_ar_peers;
+size_t mux_outproj_ar_ws_bytes(int32_t T, int32_t N, int32_t world);
+int mux_outproj_allreduce(const void* x, const void* w_packed, int32_t T, int32_t K, int32_t N,
+                          const mux_ar_peers* peers, int32_t num_sms, mux_stream_t stream);
+/* the same kernel with ALL `world` ranks' CTAs in ONE launch on this device (x[r], w_packed[r]
+ * per rank; every peers->stage / y local; peers->rank ignored): the G-rank protocol with fewer
+ * GPUs than ranks (the ranks' CTAs wait on one another, so they must share one launch, at most
+ * one CTA per SM; cooperative when the driver accepts it with clusters). */
+int mux_outproj_allreduce_emulated(const void* const* x, const void* const* w_packed, int32_t T, int32_t K,
+                                   int32_t N, const mux_ar_peers* peers, mux_stream_t stream);
+
+/* ------------------------------------------------------------------------------------
  * f4 (first part): QKV projection + RoPE + KV append, ONE kernel.
  * PAPER: each transformer layer = attention + FFN; the attention layer's projections
  * are Table 2's n d^2 terms; "attention ... generates the keys and values of new

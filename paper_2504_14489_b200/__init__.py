@@ -11,4 +11,5 @@ from .binding import (  # noqa: F401
     mux_decode_num_splits, mux_partition_configs, mux_num_prefill_layers, mux_partition_create,
     mux_run_layer, mux_device_sm_count, mux_stream_read, mux_outproj, mux_outproj_pack_w, mux_outproj_packed_bytes, PackedW, Engine, MUX_DTYPE_BF16, MUX_DTYPE_F32, SideTimes, make_side, EventSet, mux_side_plan,
     mux_rope_table, mux_qkv_rope_append, mux_ffn_pack_w13, mux_ffn_swiglu,
+    mux_outproj_ar_ws_bytes, mux_outproj_allreduce, mux_outproj_allreduce_emulated,
 )

@@ -82,6 +82,14 @@ class EngineStats(ctypes.Structure):
         return {k: getattr(self, k) for k, _ in self._fields_}
 
 
+MUX_AR_MAX_WORLD = 8
+
+
+class ArPeersC(ctypes.Structure):
+    _fields_ = [("world", c_i32), ("rank", c_i32), ("epoch", ctypes.c_uint32),
+                ("stage", c_p * MUX_AR_MAX_WORLD), ("y", c_p * MUX_AR_MAX_WORLD)]
+
+
 class SideTimes(ctypes.Structure):
     _fields_ = [("dec_start_ns", c_u64), ("dec_end_ns", c_u64), ("pf_start_ns", c_u64), ("pf_end_ns", c_u64)]
 
@@ -124,6 +132,9 @@ def lib():
         "mux_outproj": [c_p, c_p, c_p, c_i32, c_i32, c_i32, c_i32, c_p],
         "mux_outproj_sms": [c_p, c_p, c_p, c_i32, c_i32, c_i32, c_i32, c_p, c_i32],
         "mux_outproj_pack_w": [c_p, c_p, c_i32, c_i32, c_p],
+        "mux_outproj_allreduce": [c_p, c_p, c_i32, c_i32, c_i32, ctypes.POINTER(ArPeersC), c_i32, c_p],
+        "mux_outproj_allreduce_emulated": [ctypes.POINTER(c_p), ctypes.POINTER(c_p), c_i32, c_i32, c_i32,
+                                           ctypes.POINTER(ArPeersC), c_p],
         "mux_side_plan": [ctypes.POINTER(SideC), c_i32, c_p, c_i32, ctypes.POINTER(c_i32)],
         "mux_rope_table": [c_p, c_i32, c_i32, c_dbl, c_p],
         "mux_ffn_pack_w13": [c_p, c_p, c_p, c_i32, c_i32, c_p],
@@ -143,6 +154,8 @@ def lib():
         f.restype = ctypes.c_int
     L.mux_decode_workspace_bytes.argtypes = [c_i32, c_i32, c_i32, c_i32]
     L.mux_decode_workspace_bytes.restype = c_sz
+    L.mux_outproj_ar_ws_bytes.argtypes = [c_i32, c_i32, c_i32]
+    L.mux_outproj_ar_ws_bytes.restype = c_sz
     L.mux_outproj_packed_bytes.argtypes = [c_i32, c_i32]
     L.mux_outproj_packed_bytes.restype = c_sz
     L.mux_decode_num_splits.argtypes = [c_i32, c_i32, c_i32, c_p, c_i32, c_i32]
@@ -386,6 +399,40 @@ def mux_outproj(x, w: PackedW, y, stream=None, num_sms: int = 0):
     assert K == w.K and tuple(y.shape) == (T, N)
     yd = MUX_DTYPE_F32 if y.dtype == torch.float32 else MUX_DTYPE_BF16
     _check(lib().mux_outproj_sms(_ptr(x), _ptr(w.data), _ptr(y), yd, T, K, N, _stream(stream), num_sms))
+
+
+def mux_outproj_ar_ws_bytes(T: int, N: int, world: int) -> int:
+    return int(lib().mux_outproj_ar_ws_bytes(T, N, world))
+
+
+def _ar_peers(world: int, rank: int, epoch: int, stages, ys) -> ArPeersC:
+    assert 1 <= world <= MUX_AR_MAX_WORLD and len(stages) == world and len(ys) == world
+    pr = ArPeersC()
+    pr.world, pr.rank, pr.epoch = world, rank, epoch
+    for r in range(world):
+        pr.stage[r] = stages[r] if isinstance(stages[r], int) else _ptr(stages[r])
+        pr.y[r] = ys[r] if isinstance(ys[r], int) else _ptr(ys[r])
+    return pr
+
+
+def mux_outproj_allreduce(x, w: PackedW, rank: int, epoch: int, stages, ys, stream=None, num_sms: int = 0):
+    """f4: y_r = sum over ranks of x_r . W_r, the GEMM and the all-reduce in ONE kernel (include/mux.h).
+    stages / ys: per-rank staging workspaces and outputs as device addresses (ints) or tensors valid
+    in this process (peers' buffers mapped by CUDA IPC); epoch: shared launch counter, 1, 2, ..."""
+    T, K = x.shape
+    pr = _ar_peers(len(stages), rank, epoch, stages, ys)
+    _check(lib().mux_outproj_allreduce(_ptr(x), _ptr(w.data), T, K, w.N, ctypes.byref(pr), num_sms,
+                                       _stream(stream)))
+
+
+def mux_outproj_allreduce_emulated(xs, ws, epoch: int, stages, ys, stream=None):
+    """The same kernel with all len(xs) ranks' CTAs in one launch on this device (every buffer local)."""
+    G = len(xs)
+    T, K = xs[0].shape
+    pr = _ar_peers(G, 0, epoch, stages, ys)
+    xa = (c_p * G)(*[_ptr(x) for x in xs])
+    wa = (c_p * G)(*[_ptr(w.data) for w in ws])
+    _check(lib().mux_outproj_allreduce_emulated(xa, wa, T, K, ws[0].N, ctypes.byref(pr), _stream(stream)))
 
 
 def mux_device_sm_count(device: int = 0) -> int:
