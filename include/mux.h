@@ -215,6 +215,7 @@ typedef void (*mux_layer_hook)(void* user, int32_t side, int32_t layer_index, mu
 /* One side of a mux_run_layer call.  For layer i in [0, num_layers) the side processes
  * pool layer (layer0 + i) % pool_layers with inputs at base + i*stride (bytes; stride 0
  * = the same buffer every layer). */
+typedef struct mux_ar_peers mux_ar_peers;   /* f4 fused all-reduce peers, defined below */
 typedef struct {
   const mux_batch* batch;
   int32_t num_q_heads;
@@ -270,6 +271,12 @@ typedef struct {
   void* ffn_h;
   void* ffn_y;
   int32_t ffn_inter;
+  /* f4 fused communication (optional, instead of ar_fn): each layer's out-projection AND its
+   * all-reduce run as ONE mux_outproj_allreduce kernel (declared below) with these peers; layer i
+   * of the call uses epoch ar_peers->epoch + i and every rank's y shifted by i * y_stride (the same
+   * buffer layout on every rank), so the caller advances its epoch by num_layers per call.  Needs
+   * w_o, a bf16 y equal to ar_peers->y[ar_peers->rank] (layer 0), and ar_fn == NULL. */
+  const mux_ar_peers* ar_peers;
 } mux_side;
 
 /* Host-only dry run of a side's collective schedule (no GPU needed): for each layer i the side
@@ -332,16 +339,17 @@ int mux_outproj_sms(const void* x, const void* w_packed, void* y, int32_t y_dtyp
  * first call) and its Y, as addresses valid in THIS process (peers' allocations mapped by CUDA
  * IPC or VMM; rank == r: local).  Every rank calls with the same T, K, N, world and epoch.
  * num_sms: SMs the launch may use (<= 0: the device); one CTA per SM, so all of a rank's CTAs are
- * resident and the cross-rank waits cannot deadlock.  Requirements: T > 128, K and N multiples of
- * 8, 16-byte aligned buffers.  Errors: MUX_ERR_INVALID_ARG / MUX_ERR_UNSUPPORTED / MUX_ERR_CUDA. */
+ * resident and the cross-rank waits cannot deadlock.  Any T >= 1 (a decode side's few rows run in
+ * one 256-row tile; rows past T are zero-filled and never stored).  Requirements: K and N multiples
+ * of 8, 16-byte aligned buffers.  Errors: MUX_ERR_INVALID_ARG / MUX_ERR_UNSUPPORTED / MUX_ERR_CUDA. */
 #define MUX_AR_MAX_WORLD 8
-typedef struct mux_ar_peers {
+struct mux_ar_peers {
   int32_t world;
   int32_t rank;
   uint32_t epoch;
   void* stage[MUX_AR_MAX_WORLD];
   void* y[MUX_AR_MAX_WORLD];
-} mux_ar_peers;
+};
 size_t mux_outproj_ar_ws_bytes(int32_t T, int32_t N, int32_t world);
 int mux_outproj_allreduce(const void* x, const void* w_packed, int32_t T, int32_t K, int32_t N,
                           const mux_ar_peers* peers, int32_t num_sms, mux_stream_t stream);

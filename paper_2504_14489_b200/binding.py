@@ -44,6 +44,14 @@ class BatchC(ctypes.Structure):
 LayerHook = ctypes.CFUNCTYPE(None, c_p, c_i32, c_i32, c_p)
 
 
+MUX_AR_MAX_WORLD = 8
+
+
+class ArPeersC(ctypes.Structure):
+    _fields_ = [("world", c_i32), ("rank", c_i32), ("epoch", ctypes.c_uint32),
+                ("stage", c_p * MUX_AR_MAX_WORLD), ("y", c_p * MUX_AR_MAX_WORLD)]
+
+
 class SideC(ctypes.Structure):
     _fields_ = [("batch", ctypes.POINTER(BatchC)), ("num_q_heads", c_i32), ("q", c_p), ("k_new", c_p),
                 ("v_new", c_p), ("o", c_p), ("lse", c_p), ("q_stride", c_i64), ("kv_stride", c_i64),
@@ -53,7 +61,8 @@ class SideC(ctypes.Structure):
                 ("y_stride", c_i64), ("hidden", c_i32), ("y_dtype", c_i32), ("hook", LayerHook),
                 ("hook_user", c_p), ("ar_fn", c_p), ("ar_comm", c_p), ("attn_events", c_p),
                 ("x_in", c_p), ("hidden_in", c_i32), ("w_qkv", c_p), ("rope", c_p), ("rope_max_pos", c_i32),
-                ("w13", c_p), ("w2", c_p), ("ffn_h", c_p), ("ffn_y", c_p), ("ffn_inter", c_i32)]
+                ("w13", c_p), ("w2", c_p), ("ffn_h", c_p), ("ffn_y", c_p), ("ffn_inter", c_i32),
+                ("ar_peers", c_p)]
 
 
 class EngineDesc(ctypes.Structure):
@@ -80,14 +89,6 @@ class EngineStats(ctypes.Structure):
 
     def as_dict(self):
         return {k: getattr(self, k) for k, _ in self._fields_}
-
-
-MUX_AR_MAX_WORLD = 8
-
-
-class ArPeersC(ctypes.Structure):
-    _fields_ = [("world", c_i32), ("rank", c_i32), ("epoch", ctypes.c_uint32),
-                ("stage", c_p * MUX_AR_MAX_WORLD), ("y", c_p * MUX_AR_MAX_WORLD)]
 
 
 class SideTimes(ctypes.Structure):
@@ -487,7 +488,7 @@ def mux_partition_create(device: int, decode_sms: Sequence[int]) -> Partition:
 def make_side(batch: Batch, num_q_heads: int, q, o, k_new=None, v_new=None, lse=None, scale: float = 1.0,
               layer0: int = 0, num_layers: int = 1, append: bool = False, num_splits: int = 0, ws=None,
               per_layer_inputs: bool = False, w_o=None, y=None, hook=None, allreduce=None,
-              attn_events=None, qkv=None, ffn=None) -> SideC:
+              attn_events=None, qkv=None, ffn=None, ar_peers=None) -> SideC:
     """Build a mux_side.  per_layer_inputs: q/k_new/v_new/o/lse carry a leading layer dim
     and layer i uses slice i (stride = one slice); otherwise every layer reuses the buffers.
     allreduce: (fn address, comm handle) of the NCCL all-reduce the library enqueues after every
@@ -539,7 +540,12 @@ def make_side(batch: Batch, num_q_heads: int, q, o, k_new=None, v_new=None, lse=
     if ffn is not None:   # f4: (w13 PackedW, w2 PackedW, h scratch, y_ffn) -> SwiGLU FFN after out-proj
         w13, w2, fh, fy = ffn
         s.w13, s.w2, s.ffn_h, s.ffn_y, s.ffn_inter = _ptr(w13.data), _ptr(w2.data), _ptr(fh), _ptr(fy), int(w13.N // 2)
-    s._keep = (batch, q, o, k_new, v_new, lse, ws, w_o, y, cb, ev_arr, attn_events, qkv, ffn)
+    if ar_peers is not None:   # f4: (rank, epoch, stages, ys) -> out-projection + all-reduce in one kernel
+        rank, epoch, stages, ys = ar_peers
+        pr = _ar_peers(len(stages), rank, epoch, stages, ys)
+        s.ar_peers = ctypes.addressof(pr)
+        ar_peers = (ar_peers, pr)
+    s._keep = (batch, q, o, k_new, v_new, lse, ws, w_o, y, cb, ev_arr, attn_events, qkv, ffn, ar_peers)
     return s
 
 

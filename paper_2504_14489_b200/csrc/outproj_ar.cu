@@ -258,8 +258,7 @@ int ar_check(int32_t T, int32_t K, int32_t N, const mux_ar_peers* peers) {
   if (peers->world < 1 || peers->world > MUX_AR_MAX_WORLD)
     return fail(MUX_ERR_INVALID_ARG, "mux_outproj_allreduce: world must be 1..8");
   if (peers->epoch == 0) return fail(MUX_ERR_INVALID_ARG, "mux_outproj_allreduce: epoch starts at 1");
-  if (T <= 128 || K < 1 || N < 1)
-    return fail(MUX_ERR_UNSUPPORTED, "mux_outproj_allreduce: T > 128 (the CTA-pair GEMM), K, N >= 1");
+  if (T < 1 || K < 1 || N < 1) return fail(MUX_ERR_INVALID_ARG, "mux_outproj_allreduce: T, K, N must be >= 1");
   if ((K % 8) || (N % 8)) return fail(MUX_ERR_UNSUPPORTED, "mux_outproj_allreduce: K and N must be multiples of 8");
   for (int r = 0; r < peers->world; ++r) {
     if (!peers->stage[r] || !peers->y[r]) return fail(MUX_ERR_INVALID_ARG, "mux_outproj_allreduce: NULL peer buffer");

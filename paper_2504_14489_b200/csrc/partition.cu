@@ -165,7 +165,7 @@ int mux_partition_memory(mux_part_t p, int64_t* bytes) {
 namespace mux {
 // elements of the all-reduce run_side enqueues after each layer's out-projection (0 = none)
 int64_t side_allreduce_count(const mux_side* s) {
-  return (s->ar_fn && s->w_o) ? static_cast<int64_t>(s->batch->total_q) * s->hidden : 0;
+  return ((s->ar_fn || s->ar_peers) && s->w_o) ? static_cast<int64_t>(s->batch->total_q) * s->hidden : 0;
 }
 
 void launch_stamp(unsigned long long* dst, cudaStream_t st) { stamp_kernel<<<1, 1, 0, st>>>(dst); }
@@ -176,6 +176,9 @@ int run_side(mux_pool_t pool, const mux_side* s, bool decode, int sms, cudaStrea
     return fail(MUX_ERR_INVALID_ARG, "out-projection needs bf16 o, y and hidden >= 1");
   if (s->ar_fn && (!s->w_o || !s->ar_comm || s->y_dtype != MUX_DTYPE_BF16))
     return fail(MUX_ERR_INVALID_ARG, "all-reduce needs w_o, a bf16 y and ar_comm");
+  if (s->ar_peers && (!s->w_o || s->ar_fn || s->y_dtype != MUX_DTYPE_BF16 || s->ar_peers->rank < 0 ||
+                      s->ar_peers->rank >= s->ar_peers->world || s->ar_peers->y[s->ar_peers->rank] != s->y))
+    return fail(MUX_ERR_INVALID_ARG, "fused all-reduce needs w_o, a bf16 y == ar_peers->y[rank] and no ar_fn");
   if (s->w_qkv && (s->append || !s->x_in || !s->rope || s->hidden_in < 8))
     return fail(MUX_ERR_INVALID_ARG, "fused QKV needs x_in, hidden_in, rope and append == 0");
   if (s->w13 && (!s->w_o || !s->w2 || !s->ffn_h || !s->ffn_y || s->ffn_inter < 128 || s->y_dtype != MUX_DTYPE_BF16))
@@ -223,13 +226,23 @@ int run_side(mux_pool_t pool, const mux_side* s, bool decode, int sms, cudaStrea
     if ((rc = ev(i, 1))) return rc;
     if (s->w_o) {
       void* y = const_cast<void*>(at(s->y, s->y_stride));
-      rc = outproj_launch(o, at(s->w_o, s->w_stride), y, s->y_dtype, s->batch->total_q,
-                          s->num_q_heads * pool->desc.head_dim, s->hidden, reinterpret_cast<mux_stream_t>(st), sms);
-      if (rc) return rc;
-      if (ar) {
-        const int nrc = ar(y, y, static_cast<size_t>(side_allreduce_count(s)), 9 /* ncclBfloat16 */,
-                           0 /* ncclSum */, s->ar_comm, st);
-        if (nrc) return fail(MUX_ERR_CUDA, "ncclAllReduce of the out-projection failed (NCCL error " + std::to_string(nrc) + ")");
+      if (s->ar_peers) {   // f4: out-projection + all-reduce in one kernel
+        mux_ar_peers pr = *s->ar_peers;
+        pr.epoch += static_cast<uint32_t>(i);
+        for (int r = 0; r < pr.world; ++r) pr.y[r] = static_cast<uint8_t*>(pr.y[r]) + s->y_stride * i;
+        rc = mux_outproj_allreduce(o, at(s->w_o, s->w_stride), s->batch->total_q,
+                                   s->num_q_heads * pool->desc.head_dim, s->hidden, &pr, sms,
+                                   reinterpret_cast<mux_stream_t>(st));
+        if (rc) return rc;
+      } else {
+        rc = outproj_launch(o, at(s->w_o, s->w_stride), y, s->y_dtype, s->batch->total_q,
+                            s->num_q_heads * pool->desc.head_dim, s->hidden, reinterpret_cast<mux_stream_t>(st), sms);
+        if (rc) return rc;
+        if (ar) {
+          const int nrc = ar(y, y, static_cast<size_t>(side_allreduce_count(s)), 9 /* ncclBfloat16 */,
+                             0 /* ncclSum */, s->ar_comm, st);
+          if (nrc) return fail(MUX_ERR_CUDA, "ncclAllReduce of the out-projection failed (NCCL error " + std::to_string(nrc) + ")");
+        }
       }
       if (s->w13) {   // f4: the layer's FFN on the attention block's output
         rc = ffn_launch(y, s->w13, s->w2, s->ffn_h, s->ffn_y, s->batch->total_q, s->hidden, s->ffn_inter,

@@ -241,3 +241,42 @@ def test_run_layer_allreduce_enqueued_from_c(mux, part):
     finally:
         for c in comms:
             c.close()
+
+
+def test_run_layer_fused_allreduce_side(mux, part):
+    """f4 on the multiplexed path: a side with mux_side.ar_peers runs each layer's out-projection
+    and its all-reduce as ONE kernel (mux_outproj_allreduce) on the side's partition.  World 1,
+    split -1 and a real split, two consecutive calls (epochs 1 and 2): y is bitwise the standalone
+    out-projection of the side's own attention output."""
+    import torch
+    import synth
+    Hq, Hkv, d, hidden = 8, 2, 128, 256
+    pf, dc, pool, g_pf, g_dc = _workload(mux, Hq, Hkv, d)
+    wo_bits = synth.make_wo(803, Shapes(Hq, Hkv, d, 1, hidden=hidden))
+    w_o = mux.mux_outproj_pack_w(torch.from_numpy(wo_bits.view(np.int16)).cuda().view(torch.bfloat16))
+    st_pf = torch.zeros(mux.mux_outproj_ar_ws_bytes(429, hidden, 1), dtype=torch.uint8, device="cuda")
+    st_dc = torch.zeros(mux.mux_outproj_ar_ws_bytes(3, hidden, 1), dtype=torch.uint8, device="cuda")
+    epoch = 1
+    for split in (-1, 0):
+        ws = torch.empty(max(16, mux.mux_decode_workspace_bytes(3, Hq, d, 2)), dtype=torch.uint8, device="cuda")
+        o_pf = torch.empty((429, Hq, d), dtype=torch.bfloat16, device="cuda")
+        o_dc = torch.empty((3, Hq, d), dtype=torch.bfloat16, device="cuda")
+        y_pf = torch.full((429, hidden), float("nan"), dtype=torch.bfloat16, device="cuda")
+        y_dc = torch.full((3, hidden), float("nan"), dtype=torch.bfloat16, device="cuda")
+        s_pf = mux.make_side(g_pf["batch"], Hq, g_pf["q"], o_pf, scale=1 / math.sqrt(d), num_layers=1,
+                             w_o=w_o, y=y_pf, ar_peers=(0, epoch, [st_pf], [y_pf]))
+        s_dc = mux.make_side(g_dc["batch"], Hq, g_dc["q"], o_dc, scale=1 / math.sqrt(d), num_splits=2, ws=ws,
+                             num_layers=1, w_o=w_o, y=y_dc, ar_peers=(0, epoch, [st_dc], [y_dc]))
+        assert (mux.mux_side_plan(s_pf, pool.desc.num_layers)[:, 1] == 429 * hidden).all()
+        mux.mux_run_layer(part, split, pool, s_pf, s_dc, None)
+        torch.cuda.synchronize()
+        epoch += 1
+        for o, y, exact in ((o_pf, y_pf, True), (o_dc, y_dc, False)):
+            y2 = torch.empty_like(y)
+            mux.mux_outproj(o.view(o.shape[0], -1), w_o, y2)   # 3 rows: the skinny (transposed) GEMM
+            torch.cuda.synchronize()
+            assert not torch.isnan(y.float()).any(), f"split {split}"
+            if exact:
+                assert torch.equal(y.view(torch.int16), y2.view(torch.int16)), f"split {split}"
+            else:   # same fp32 products, another MMA shape: within one bf16 rounding
+                assert ((y.float() - y2.float()).abs() <= 2.0 ** -8 * y2.float().abs() + 1e-3).all(), f"split {split}"

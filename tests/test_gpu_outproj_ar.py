@@ -66,6 +66,7 @@ def _run(mux, G, T, K, N, epochs=2):
     (3, 520, 136, 776),      # a world that does not divide the tile count
     (4, 1024, 512, 1024),
     (8, 640, 128, 1032),     # TP-8: more ranks than tiles of some owners
+    (8, 64, 1024, 1024),     # a decode side's rows (one partial M tile), 70B TP-8 out-projection K
 ])
 def test_fused_allreduce_matches_oracle(mux, G, T, K, N):
     import torch
@@ -121,4 +122,4 @@ def test_fused_allreduce_rejects_bad_args(mux):
     with pytest.raises(mux.MuxError):
         mux.mux_outproj_allreduce(x, w, 0, 0, [st], [y])          # epoch starts at 1
     with pytest.raises(mux.MuxError):
-        mux.mux_outproj_allreduce(x[:128], w, 0, 1, [st], [y])    # T <= 128: the skinny path has no fused AR
+        mux.mux_outproj_allreduce(x, w, 1, 1, [st], [y])          # rank outside the world
