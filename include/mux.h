@@ -273,8 +273,9 @@ typedef struct {
   int32_t ffn_inter;
   /* f4 fused communication (optional, instead of ar_fn): each layer's out-projection AND its
    * all-reduce run as ONE mux_outproj_allreduce kernel (declared below) with these peers; layer i
-   * of the call uses epoch ar_peers->epoch + i and every rank's y shifted by i * y_stride (the same
-   * buffer layout on every rank), so the caller advances its epoch by num_layers per call.  Needs
+   * of the call uses every rank's y shifted by i * y_stride (the same buffer layout on every rank)
+   * and epoch 0 (automatic) or, when ar_peers->epoch != 0, ar_peers->epoch + i (the caller then
+   * advances its epoch by num_layers per call).  Needs
    * w_o, a bf16 y equal to ar_peers->y[ar_peers->rank] (layer 0), and ar_fn == NULL. */
   const mux_ar_peers* ar_peers;
 } mux_side;
@@ -333,8 +334,10 @@ int mux_outproj_sms(const void* x, const void* w_packed, void* y, int32_t y_dtyp
  * rank; the kernel returns once this rank's Y is complete.  Traffic per rank equals a ring
  * all-reduce's (2 (G-1)/G of Y), but it leaves the GPU tile by tile during the GEMM.
  *
- * peers: world G (1..MUX_AR_MAX_WORLD), this rank, epoch (launch counter shared by all ranks:
- * 1 on the first call with a workspace, +1 per call; counters are never reset) and, per rank r,
+ * peers: world G (1..MUX_AR_MAX_WORLD), this rank, epoch (0 = automatic: the kernel keeps a launch
+ * counter in the rank's own workspace, so repeated calls and CUDA-graph replays need nothing from
+ * the host; else an explicit counter shared by all ranks, 1 on the first call with a workspace, +1
+ * per call; the two modes must not be mixed on one workspace; counters are never reset) and, per rank r,
  * its staging workspace (mux_outproj_ar_ws_bytes(T, N, G) bytes, zero-filled ONCE before the
  * first call) and its Y, as addresses valid in THIS process (peers' allocations mapped by CUDA
  * IPC or VMM; rank == r: local).  Every rank calls with the same T, K, N, world and epoch.
@@ -343,6 +346,15 @@ int mux_outproj_sms(const void* x, const void* w_packed, void* y, int32_t y_dtyp
  * one 256-row tile; rows past T are zero-filled and never stored).  Requirements: K and N multiples
  * of 8, 16-byte aligned buffers.  Errors: MUX_ERR_INVALID_ARG / MUX_ERR_UNSUPPORTED / MUX_ERR_CUDA. */
 #define MUX_AR_MAX_WORLD 8
+#define MUX_IPC_HANDLE_BYTES 64
+/* peer buffers for it: device memory another process can map through CUDA IPC.  mux_ipc_alloc:
+ * cudaMalloc'd, zero-filled, its 64-byte handle written to `handle` (exchange it with the other
+ * ranks, e.g. torch.distributed.all_gather_object); mux_ipc_open maps another process's handle
+ * (not this process's own: use the local pointer for your rank); mux_ipc_close / mux_ipc_free undo them. */
+int mux_ipc_alloc(size_t bytes, void** ptr, void* handle);
+int mux_ipc_open(const void* handle, void** ptr);
+int mux_ipc_close(void* ptr);
+int mux_ipc_free(void* ptr);
 struct mux_ar_peers {
   int32_t world;
   int32_t rank;

@@ -136,6 +136,10 @@ def lib():
         "mux_outproj_allreduce": [c_p, c_p, c_i32, c_i32, c_i32, ctypes.POINTER(ArPeersC), c_i32, c_p],
         "mux_outproj_allreduce_emulated": [ctypes.POINTER(c_p), ctypes.POINTER(c_p), c_i32, c_i32, c_i32,
                                            ctypes.POINTER(ArPeersC), c_p],
+        "mux_ipc_alloc": [c_sz, ctypes.POINTER(c_p), c_p],
+        "mux_ipc_open": [c_p, ctypes.POINTER(c_p)],
+        "mux_ipc_close": [c_p],
+        "mux_ipc_free": [c_p],
         "mux_side_plan": [ctypes.POINTER(SideC), c_i32, c_p, c_i32, ctypes.POINTER(c_i32)],
         "mux_rope_table": [c_p, c_i32, c_i32, c_dbl, c_p],
         "mux_ffn_pack_w13": [c_p, c_p, c_p, c_i32, c_i32, c_p],
@@ -414,6 +418,49 @@ def _ar_peers(world: int, rank: int, epoch: int, stages, ys) -> ArPeersC:
         pr.stage[r] = stages[r] if isinstance(stages[r], int) else _ptr(stages[r])
         pr.y[r] = ys[r] if isinstance(ys[r], int) else _ptr(ys[r])
     return pr
+
+
+class IpcBuffer:
+    """Device memory shareable through CUDA IPC (mux_ipc_alloc); `handle` (64 bytes) maps it in
+    another process with IpcBuffer.open(handle).  `tensor(shape, dtype)` views it as a torch tensor."""
+
+    def __init__(self, nbytes: int = 0, handle: bytes | None = None):
+        self.ptr = c_p()
+        if handle is None:
+            h = ctypes.create_string_buffer(64)
+            _check(lib().mux_ipc_alloc(nbytes, ctypes.byref(self.ptr), h))
+            self.handle, self.owned, self.nbytes = h.raw, True, nbytes
+        else:
+            _check(lib().mux_ipc_open(handle, ctypes.byref(self.ptr)))
+            self.handle, self.owned, self.nbytes = handle, False, nbytes
+
+    @classmethod
+    def open(cls, handle: bytes, nbytes: int):
+        return cls(nbytes, handle)
+
+    @property
+    def address(self) -> int:
+        return int(self.ptr.value or 0)
+
+    def tensor(self, shape, dtype):
+        import torch
+        n = 1
+        for x in shape:
+            n *= int(x)
+        itemsize = torch.empty((), dtype=dtype).element_size()
+        assert n * itemsize <= self.nbytes
+        typestr = {torch.bfloat16: "<i2", torch.uint8: "|u1", torch.float32: "<f4"}[dtype]
+
+        class _Iface:
+            __cuda_array_interface__ = {"shape": tuple(int(x) for x in shape), "typestr": typestr,
+                                        "data": (self.address, False), "version": 3}
+        t = torch.as_tensor(_Iface(), device="cuda")
+        return t.view(dtype) if dtype == torch.bfloat16 else t
+
+    def close(self):
+        if self.address:
+            _check(lib().mux_ipc_free(self.ptr) if self.owned else lib().mux_ipc_close(self.ptr))
+            self.ptr = c_p()
 
 
 def mux_outproj_allreduce(x, w: PackedW, rank: int, epoch: int, stages, ys, stream=None, num_sms: int = 0):

@@ -21,7 +21,8 @@
 //     stores), then count the half tile on every rank's done counter.
 //   phase 3: the first CTA of each rank waits until its done counter shows all 2 x tiles half
 //     tiles of the launch: the kernel ends with this rank's Y complete.
-// Counters are never reset: launch number `epoch` (1, 2, ...) waits for epoch x count.
+// Counters are never reset: launch number `epoch` (1, 2, ...) waits for epoch x count; epoch 0 in
+// the call = take it from the rank's own launch counter in the workspace (CUDA-graph friendly).
 // Deadlock freedom: phase 1 waits on nothing remote, phase 2 only on phase 1 of other ranks,
 // phase 3 only on phase 2; every rank's grid fits its SMs (one CTA per SM, all co-resident).
 // With fewer GPUs than ranks the same kernel runs ALL ranks' CTAs in one launch on one device
@@ -61,7 +62,7 @@ struct ArParams {
   uint16_t* y[MUX_AR_MAX_WORLD];
 };
 
-// staging of one rank: [nslots][G][256][256] bf16, then uint32 counters [nslots] and done
+// staging of one rank: [nslots][G][256][256] bf16, then uint32 counters [nslots], done, launches
 __host__ __device__ inline size_t ar_stage_elems(int nslots, int G) {
   return static_cast<size_t>(nslots) * G * kArTileElems;
 }
@@ -101,6 +102,10 @@ __global__ void __launch_bounds__(kArThreads, 1)
   const int ntiles128 = (p.N + 127) / 128;
   const CUtensorMap* tmx = &maps.x[rl];
   const CUtensorMap* tmw = &maps.w[rl];
+  // epoch 0 = automatic: this rank's launch counter (the word after `done`, bumped by CTA 0 at the
+  // end of every launch; the next launch on the stream reads it after this kernel completed)
+  uint32_t* my_words = ar_flags(p, rank);
+  const uint32_t epoch = p.epoch ? p.epoch : *reinterpret_cast<volatile uint32_t*>(my_words + p.nslots + 1) + 1;
 
   if (threadIdx.x == 0) {
     for (int i = 0; i < 2 * kArStages + 2; ++i) dev::mbar_init(&full[i], 1);
@@ -205,8 +210,8 @@ __global__ void __launch_bounds__(kArThreads, 1)
     // phase 2: the half tiles this rank owns, over this rank's CTAs
     const int cid = pair * 2 + static_cast<int>(crank), ncta = 2 * p.pairs;
     const int nown = rank < p.tiles ? (p.tiles - rank + G - 1) / G : 0;
-    uint32_t* my_flags = ar_flags(p, rank);
-    const uint32_t need = p.epoch * static_cast<uint32_t>(2 * G);
+    uint32_t* my_flags = my_words;
+    const uint32_t need = epoch * static_cast<uint32_t>(2 * G);
     for (int u = cid; u < 2 * nown; u += ncta) {
       const int s = u >> 1, half = u & 1;
       const int t = s * G + rank;
@@ -242,7 +247,12 @@ __global__ void __launch_bounds__(kArThreads, 1)
       }
     }
     // phase 3: this rank's Y is complete once every half tile of the launch was counted here
-    if (cid == 0 && threadIdx.x == 0) wait_count(my_flags + p.nslots, p.epoch * static_cast<uint32_t>(2 * p.tiles));
+    // (every CTA of this rank read the launch counter before its phase-1 arrivals, which the
+    // waits below imply, so CTA 0 may bump it afterwards)
+    if (cid == 0 && threadIdx.x == 0) {
+      wait_count(my_flags + p.nslots, epoch * static_cast<uint32_t>(2 * p.tiles));
+      if (!p.epoch) my_flags[p.nslots + 1] = epoch;
+    }
   }
   dev::tc_fence_before();
   __syncthreads();
@@ -257,7 +267,6 @@ int ar_check(int32_t T, int32_t K, int32_t N, const mux_ar_peers* peers) {
   if (!peers) return fail(MUX_ERR_INVALID_ARG, "mux_outproj_allreduce: peers NULL");
   if (peers->world < 1 || peers->world > MUX_AR_MAX_WORLD)
     return fail(MUX_ERR_INVALID_ARG, "mux_outproj_allreduce: world must be 1..8");
-  if (peers->epoch == 0) return fail(MUX_ERR_INVALID_ARG, "mux_outproj_allreduce: epoch starts at 1");
   if (T < 1 || K < 1 || N < 1) return fail(MUX_ERR_INVALID_ARG, "mux_outproj_allreduce: T, K, N must be >= 1");
   if ((K % 8) || (N % 8)) return fail(MUX_ERR_UNSUPPORTED, "mux_outproj_allreduce: K and N must be multiples of 8");
   for (int r = 0; r < peers->world; ++r) {
@@ -345,7 +354,7 @@ extern "C" size_t mux_outproj_ar_ws_bytes(int32_t T, int32_t N, int32_t world) {
   if (T < 1 || N < 1 || world < 1 || world > MUX_AR_MAX_WORLD) return 0;
   const int tiles = ((T + 2 * kArBM - 1) / (2 * kArBM)) * ((N + kArBN - 1) / kArBN);
   const int nslots = (tiles + world - 1) / world;
-  return ar_stage_elems(nslots, world) * 2 + (static_cast<size_t>(nslots) + 1) * 4;
+  return ar_stage_elems(nslots, world) * 2 + (static_cast<size_t>(nslots) + 2) * 4;
 }
 
 extern "C" int mux_outproj_allreduce(const void* x, const void* w_packed, int32_t T, int32_t K, int32_t N,
@@ -373,4 +382,43 @@ extern "C" int mux_outproj_allreduce_emulated(const void* const* x, const void* 
   ArParams prm = ar_params(T, K, N, peers);
   prm.rank0 = 0;
   return ar_launch(maps, prm, peers->world, device_sm_count(), true, reinterpret_cast<cudaStream_t>(stream));
+}
+
+extern "C" int mux_ipc_alloc(size_t bytes, void** ptr, void* handle) {
+  if (!ptr || !handle || bytes == 0) return fail(MUX_ERR_INVALID_ARG, "mux_ipc_alloc: bad argument");
+  *ptr = nullptr;
+  void* p = nullptr;
+  MUX_CUDA(cudaMalloc(&p, bytes));
+  cudaError_t e = cudaMemset(p, 0, bytes);
+  cudaIpcMemHandle_t h;
+  if (e == cudaSuccess) e = cudaIpcGetMemHandle(&h, p);
+  if (e != cudaSuccess) {
+    cudaFree(p);
+    return cuda_fail(e, "mux_ipc_alloc");
+  }
+  static_assert(sizeof(cudaIpcMemHandle_t) == MUX_IPC_HANDLE_BYTES, "IPC handle size");
+  memcpy(handle, &h, sizeof(h));
+  *ptr = p;
+  return MUX_OK;
+}
+
+extern "C" int mux_ipc_open(const void* handle, void** ptr) {
+  if (!ptr || !handle) return fail(MUX_ERR_INVALID_ARG, "mux_ipc_open: bad argument");
+  cudaIpcMemHandle_t h;
+  memcpy(&h, handle, sizeof(h));
+  *ptr = nullptr;
+  MUX_CUDA(cudaIpcOpenMemHandle(ptr, h, cudaIpcMemLazyEnablePeerAccess));
+  return MUX_OK;
+}
+
+extern "C" int mux_ipc_close(void* ptr) {
+  if (!ptr) return MUX_OK;
+  MUX_CUDA(cudaIpcCloseMemHandle(ptr));
+  return MUX_OK;
+}
+
+extern "C" int mux_ipc_free(void* ptr) {
+  if (!ptr) return MUX_OK;
+  MUX_CUDA(cudaFree(ptr));
+  return MUX_OK;
 }

@@ -228,7 +228,7 @@ int run_side(mux_pool_t pool, const mux_side* s, bool decode, int sms, cudaStrea
       void* y = const_cast<void*>(at(s->y, s->y_stride));
       if (s->ar_peers) {   // f4: out-projection + all-reduce in one kernel
         mux_ar_peers pr = *s->ar_peers;
-        pr.epoch += static_cast<uint32_t>(i);
+        if (pr.epoch) pr.epoch += static_cast<uint32_t>(i);   // explicit epochs; 0 = the kernel's counter
         for (int r = 0; r < pr.world; ++r) pr.y[r] = static_cast<uint8_t*>(pr.y[r]) + s->y_stride * i;
         rc = mux_outproj_allreduce(o, at(s->w_o, s->w_stride), s->batch->total_q,
                                    s->num_q_heads * pool->desc.head_dim, s->hidden, &pr, sms,

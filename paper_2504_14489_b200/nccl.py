@@ -98,3 +98,46 @@ class Comm:
         if self.comm:
             lib().ncclCommDestroy(self.comm)
             self.comm = ctypes.c_void_p()
+
+
+class PeerSet:
+    """f4 fused all-reduce buffers (include/mux.h mux_outproj_allreduce): this rank's staging
+    workspace and output Y allocated for CUDA IPC, their handles exchanged over the default
+    torch.distributed group (any backend), and every other rank's buffers mapped into this
+    process.  `peers()` gives the (rank, epoch, stages, ys) tuple for make_side(ar_peers=...)
+    with epoch 0 (the kernel's own launch counter).  The fused kernel needs every rank on its
+    own GPU (its CTAs wait on the other ranks' stores)."""
+
+    def __init__(self, rank: int, world: int, T: int, N: int):
+        import torch
+        import torch.distributed as dist
+        from .binding import IpcBuffer, mux_outproj_ar_ws_bytes
+        self.rank, self.world, self.T, self.N = rank, world, T, N
+        ws_bytes = mux_outproj_ar_ws_bytes(T, N, world)
+        y_bytes = T * N * 2
+        self.mine = [IpcBuffer(ws_bytes), IpcBuffer(y_bytes)]
+        handles = [(self.mine[0].handle, self.mine[1].handle)]
+        if world > 1:
+            allh = [None] * world
+            dist.all_gather_object(allh, handles[0])
+            handles = allh
+        self.opened = []
+        self.stage_addr, self.y_addr, self.y_bufs = [], [], []
+        for r in range(world):
+            if r == rank:
+                st, y = self.mine
+            else:
+                st, y = IpcBuffer.open(handles[r][0], ws_bytes), IpcBuffer.open(handles[r][1], y_bytes)
+                self.opened += [st, y]
+            self.stage_addr.append(st.address)
+            self.y_addr.append(y.address)
+            self.y_bufs.append(y)
+        self.y = self.mine[1].tensor((T, N), torch.bfloat16)   # this rank's reduced output
+
+    def peers(self):
+        return (self.rank, 0, list(self.stage_addr), list(self.y_addr))
+
+    def close(self):
+        for b in self.opened + self.mine:
+            b.close()
+        self.opened, self.mine, self.y_bufs = [], [], []
