@@ -189,6 +189,7 @@ class Workload:
         self.pf_y = torch.empty((Tp, self.hidden), dtype=torch.bfloat16, device=dev)
         self.dc_y = torch.empty((Bd, self.hidden), dtype=torch.bfloat16, device=dev)
         self.ar = {}
+        self.ar_peers = {}
         self.scale = 1.0 / math.sqrt(self.d)
         self.ws = None
 
@@ -205,10 +206,12 @@ class Workload:
             self.ws = torch.empty(max(16, wsb), dtype=torch.uint8, device="cuda")
         pf = mux.make_side(self.pf_batch, self.Hq, self.pf_q, self.pf_o, k_new=self.pf_k, v_new=self.pf_v,
                            scale=self.scale, layer0=0, num_layers=self.layers, append=True,
-                           w_o=self.w_o, y=self.pf_y, allreduce=self.ar.get(1), attn_events=pf_events)
+                           w_o=self.w_o, y=self.pf_y, allreduce=self.ar.get(1), ar_peers=self.ar_peers.get(1),
+                           attn_events=pf_events)
         dc = mux.make_side(self.dc_batch, self.Hq, self.dc_q, self.dc_o, k_new=self.dc_k, v_new=self.dc_v,
                            scale=self.scale, layer0=dc_layer0 % self.layers, num_layers=dc_layers, append=True,
                            num_splits=ns, ws=self.ws, w_o=self.w_o, y=self.dc_y, allreduce=self.ar.get(0),
+                           ar_peers=self.ar_peers.get(0),
                            attn_events=dc_events)
         return pf, dc, ns
 
@@ -216,6 +219,16 @@ class Workload:
         """Per-layer all-reduce of each side's out-projection partial sums (a7, R23), enqueued by
         libmux from C on the side's own stream through one NCCL communicator per side."""
         self.ar = {0: comms[0].c_allreduce(), 1: comms[1].c_allreduce()}
+
+    def set_fused_allreduce(self, rank: int, world: int):
+        """f4: each layer's out-projection AND its all-reduce as ONE kernel over peer memory
+        (mux_side.ar_peers, CUDA IPC buffers exchanged over torch.distributed); y lives in the
+        IPC-shared buffer the other ranks store their reduced tiles into."""
+        from paper_2504_14489_b200 import nccl
+        self.peer_sets = [nccl.PeerSet(rank, world, self.dc_y.shape[0], self.hidden),
+                          nccl.PeerSet(rank, world, self.pf_y.shape[0], self.hidden)]
+        self.dc_y, self.pf_y = self.peer_sets[0].y, self.peer_sets[1].y
+        self.ar_peers = {0: self.peer_sets[0].peers(), 1: self.peer_sets[1].peers()}
 
     def outproj_flops_layer(self, side):
         return 2.0 * side.total_new * self.Hq * self.d * self.hidden
@@ -483,12 +496,13 @@ def model_step(mux, part, wl, NT, tbt_slo_ms, total_sms, inter=14336, reps=3):
         pf, dc, _ = wl.sides(dsms, D, l0)
         x, h, y = bufs["pf"]
         pf = mux.make_side(wl.pf_batch, wl.Hq, wl.pf_q, wl.pf_o, scale=wl.scale, layer0=0, num_layers=NT, w_o=wl.w_o,
-                           y=wl.pf_y, allreduce=wl.ar.get(1), qkv=(x, w_qkv, rope), ffn=(w13, w2, h, y))
+                           y=wl.pf_y, allreduce=wl.ar.get(1), ar_peers=wl.ar_peers.get(1), qkv=(x, w_qkv, rope),
+                           ffn=(w13, w2, h, y))
         x, h, y = bufs["dc"]
         ns = mux.mux_decode_num_splits(B, wl.Hkv, max(wl.dc_spec.L), dsms, wl.dc_spec.L, wl.d)
         dc = mux.make_side(wl.dc_batch, wl.Hq, wl.dc_q, wl.dc_o, scale=wl.scale, layer0=l0 % NT, num_layers=D,
                            num_splits=ns, ws=wl.ws, w_o=wl.w_o, y=wl.dc_y, allreduce=wl.ar.get(0),
-                           qkv=(x, w_qkv, rope), ffn=(w13, w2, h, y))
+                           ar_peers=wl.ar_peers.get(0), qkv=(x, w_qkv, rope), ffn=(w13, w2, h, y))
         return pf, dc
 
     def timed(i, pf, dc, n=reps):
@@ -611,6 +625,9 @@ def main():
                     help="decode TBT SLO the chosen split must meet (default: P:734, 50 ms for Llama3-8B "
                          "shapes, 100 ms for Llama3-70B)")
     ap.add_argument("--no-model-step", action="store_true", help="skip the full-layer (f4) step")
+    ap.add_argument("--ar", default="nccl", choices=["nccl", "fused"],
+                    help="out-projection all-reduce: NCCL call per layer (a7), or the fused GEMM + "
+                         "all-reduce kernel over CUDA-IPC peer memory (f4); fused also runs at N=1")
     ap.add_argument("--oracle-1thread", action="store_true", help=argparse.SUPPRESS)
     args = ap.parse_args()
     args.warmup = max(3, args.warmup)
@@ -643,12 +660,15 @@ def main():
     wl = Workload(args.config, rank, world, layers=args.layers or None)
     NT = wl.layers
     comms = []
+    if args.ar == "fused":
+        wl.set_fused_allreduce(rank, world)
     if world > 1:
-        # one NCCL communicator per side; libmux enqueues each layer's all-reduce of the out-proj
-        # partial sums from C on the side's own (green-context) stream (mux_side.ar_fn / ar_comm)
-        from paper_2504_14489_b200 import nccl
-        comms = [nccl.Comm(rank, world), nccl.Comm(rank, world)]
-        wl.set_allreduce(comms)
+        if args.ar == "nccl":
+            # one NCCL communicator per side; libmux enqueues each layer's all-reduce of the out-proj
+            # partial sums from C on the side's own (green-context) stream (mux_side.ar_fn / ar_comm)
+            from paper_2504_14489_b200 import nccl
+            comms = [nccl.Comm(rank, world), nccl.Comm(rank, world)]
+            wl.set_allreduce(comms)
         h = torch.tensor([wl.page_hash], device="cuda")   # identical page tables on every rank
         hs = [torch.zeros_like(h) for _ in range(world)]
         dist.all_gather(hs, h)
@@ -796,6 +816,8 @@ def main():
     for k in names_in + ("pf_o", "dc_o", "pf_y", "dc_y"):
         setattr(wl2, k, torch.empty_like(getattr(wl, k)))
     wl2.ws = None
+    if args.ar == "fused":
+        wl2.set_fused_allreduce(rank, world)                # its own peer-shared y / staging
     sets = [wl, wl2]
     e2e_sides = {}
 
@@ -944,6 +966,8 @@ def main():
                    "decode_layers_per_step": D, "decode_iters_per_step": D / NT,
                    "tbt_slo_ms": args.tbt_slo_ms, "tbt_ms": t_step * 1e3 * NT / D,
                    "decode_num_splits": ns, "parallelism": f"kv-head shard x{world}" if world > 1 else "single GPU",
+                   "allreduce": ("fused out-proj GEMM + all-reduce kernel (peer memory)" if args.ar == "fused"
+                                 else "NCCL all-reduce per layer" if world > 1 else "none (one rank)"),
                    "l2": ("L2 flushed (256 MB write) before every timed step" if flush is not None else
                           "inputs larger than L2 (KV pool of every layer >> 126 MB; layers rotate)")},
         "roofline": roofline, "roofline_decode": roofline_dec,

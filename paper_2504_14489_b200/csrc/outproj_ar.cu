@@ -172,7 +172,61 @@ __global__ void __launch_bounds__(kArThreads, 1)
   } else {
     // ---------------------------------------------------------------- epilogue warps 0-3
     const int G = p.G;
-    // phase 1: my 128 rows of each tile -> bf16 -> the owner's staging slot, then count it there
+    // the half tiles (units) this rank owns, spread over its CTAs: unit u = (slot u / 2, half u % 2)
+    const int cid = pair * 2 + static_cast<int>(crank), ncta = 2 * p.pairs;
+    const int nown = rank < p.tiles ? (p.tiles - rank + G - 1) / G : 0;
+    uint32_t* my_flags = my_words;
+    const uint32_t need = epoch * static_cast<uint32_t>(2 * G);
+    int next_u = cid;
+    // sum the G partials of one unit in rank order (fp32), round to bf16, store into every rank's Y,
+    // count it on every rank.  Each warp takes 32 rows in batches of 8 (8 independent 16-byte loads
+    // per rank in flight per lane); lane = 8 columns.
+    auto reduce_unit = [&](int u) {
+      const int s = u >> 1, half = u & 1;
+      const int t = s * G + rank;
+      const int m0 = (t / p.n_tiles) * 2 * kArBM, n0 = (t % p.n_tiles) * kArBN;
+      const uint16_t* src = p.stage[rank] + static_cast<size_t>(s) * G * kArTileElems;
+      const int col = n0 + 8 * lane;
+#pragma unroll 1
+      for (int rb = 0; rb < 32; rb += 8) {
+        float acc[8][8];
+#pragma unroll
+        for (int k = 0; k < 8; ++k)
+#pragma unroll
+          for (int e = 0; e < 8; ++e) acc[k][e] = 0.f;
+        for (int r = 0; r < G; ++r) {             // rank order: the same sum on every rank
+          uint4 v[8];
+#pragma unroll
+          for (int k = 0; k < 8; ++k)
+            v[k] = __ldcg(reinterpret_cast<const uint4*>(src + static_cast<size_t>(r) * kArTileElems +
+                                                           static_cast<size_t>(half * kArBM + warp * 32 + rb + k) * kArBN +
+                                                           8 * lane));
+#pragma unroll
+          for (int k = 0; k < 8; ++k) {
+            acc[k][0] += dev::bf16lo(v[k].x); acc[k][1] += dev::bf16hi(v[k].x);
+            acc[k][2] += dev::bf16lo(v[k].y); acc[k][3] += dev::bf16hi(v[k].y);
+            acc[k][4] += dev::bf16lo(v[k].z); acc[k][5] += dev::bf16hi(v[k].z);
+            acc[k][6] += dev::bf16lo(v[k].w); acc[k][7] += dev::bf16hi(v[k].w);
+          }
+        }
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+          const int row = m0 + half * kArBM + warp * 32 + rb + k;
+          if (row < p.T && col < p.N) {
+            const uint4 o = make_uint4(dev::pack_bf16(acc[k][0], acc[k][1]), dev::pack_bf16(acc[k][2], acc[k][3]),
+                                       dev::pack_bf16(acc[k][4], acc[k][5]), dev::pack_bf16(acc[k][6], acc[k][7]));
+            for (int r = 0; r < G; ++r) *reinterpret_cast<uint4*>(p.y[r] + static_cast<size_t>(row) * p.N + col) = o;
+          }
+        }
+      }
+      dev::named_bar_sync(1, 128);
+      if (threadIdx.x == 0) {
+        fence_sys();
+        for (int r = 0; r < G; ++r) red_add_sys(ar_flags(p, r) + p.nslots, 1u);
+      }
+    };
+    // phase 1: my 128 rows of each tile -> bf16 -> the owner's staging slot, then count it there;
+    // between tiles (while the MMA fills the other accumulator) reduce owned units that are ready
     int i = 0;
     for (int t = pair; t < p.tiles; t += p.pairs, ++i) {
       const int b = i & 1;
@@ -206,45 +260,22 @@ __global__ void __launch_bounds__(kArThreads, 1)
         fence_sys();
         red_add_sys(ar_flags(p, owner) + slot, 1u);
       }
+      // overlap: at most two ready units per tile (the next accumulator must not wait long)
+      for (int k = 0; k < 2 && next_u < 2 * nown; ++k) {
+        const bool ready = dev::bar_red_or(1, 128, threadIdx.x == 0 &&
+                                                       static_cast<int32_t>(ld_acquire_sys(my_flags + (next_u >> 1)) - need) >= 0);
+        if (!ready) break;
+        reduce_unit(next_u);
+        next_u += ncta;
+      }
     }
-    // phase 2: the half tiles this rank owns, over this rank's CTAs
-    const int cid = pair * 2 + static_cast<int>(crank), ncta = 2 * p.pairs;
-    const int nown = rank < p.tiles ? (p.tiles - rank + G - 1) / G : 0;
-    uint32_t* my_flags = my_words;
-    const uint32_t need = epoch * static_cast<uint32_t>(2 * G);
-    for (int u = cid; u < 2 * nown; u += ncta) {
-      const int s = u >> 1, half = u & 1;
-      const int t = s * G + rank;
-      const int m0 = (t / p.n_tiles) * 2 * kArBM, n0 = (t % p.n_tiles) * kArBN;
+    // phase 2 (the remaining half tiles this rank owns; blocking waits)
+    while (next_u < 2 * nown) {
+      const int s = next_u >> 1;
       if (threadIdx.x == 0) wait_count(my_flags + s, need);
       dev::named_bar_sync(1, 128);
-      const uint16_t* src = p.stage[rank] + static_cast<size_t>(s) * G * kArTileElems;
-      const int col = n0 + 8 * lane;
-#pragma unroll 1
-      for (int rr = 0; rr < 32; ++rr) {
-        const int rloc = half * kArBM + warp * 32 + rr;
-        const int row = m0 + rloc;
-        float acc[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
-        for (int r = 0; r < G; ++r) {             // rank order: the same sum on every rank
-          const uint4 v = __ldcg(reinterpret_cast<const uint4*>(src + static_cast<size_t>(r) * kArTileElems +
-                                                                  static_cast<size_t>(rloc) * kArBN + 8 * lane));
-          acc[0] += dev::bf16lo(v.x); acc[1] += dev::bf16hi(v.x);
-          acc[2] += dev::bf16lo(v.y); acc[3] += dev::bf16hi(v.y);
-          acc[4] += dev::bf16lo(v.z); acc[5] += dev::bf16hi(v.z);
-          acc[6] += dev::bf16lo(v.w); acc[7] += dev::bf16hi(v.w);
-        }
-        if (row < p.T && col < p.N) {
-          const uint4 o = make_uint4(dev::pack_bf16(acc[0], acc[1]), dev::pack_bf16(acc[2], acc[3]),
-                                     dev::pack_bf16(acc[4], acc[5]), dev::pack_bf16(acc[6], acc[7]));
-          for (int r = 0; r < G; ++r)
-            *reinterpret_cast<uint4*>(p.y[r] + static_cast<size_t>(row) * p.N + col) = o;
-        }
-      }
-      dev::named_bar_sync(1, 128);
-      if (threadIdx.x == 0) {
-        fence_sys();
-        for (int r = 0; r < G; ++r) red_add_sys(ar_flags(p, r) + p.nslots, 1u);
-      }
+      reduce_unit(next_u);
+      next_u += ncta;
     }
     // phase 3: this rank's Y is complete once every half tile of the launch was counted here
     // (every CTA of this rank read the launch counter before its phase-1 arrivals, which the
