@@ -625,9 +625,9 @@ def main():
                     help="decode TBT SLO the chosen split must meet (default: P:734, 50 ms for Llama3-8B "
                          "shapes, 100 ms for Llama3-70B)")
     ap.add_argument("--no-model-step", action="store_true", help="skip the full-layer (f4) step")
-    ap.add_argument("--ar", default="nccl", choices=["nccl", "fused"],
-                    help="out-projection all-reduce: NCCL call per layer (a7), or the fused GEMM + "
-                         "all-reduce kernel over CUDA-IPC peer memory (f4); fused also runs at N=1")
+    ap.add_argument("--ar", default=None, choices=["nccl", "fused"],
+                    help="out-projection all-reduce: the fused GEMM + all-reduce kernel over CUDA-IPC peer "
+                         "memory (f4; default at N>1, also runs at N=1), or an NCCL call per layer (a7)")
     ap.add_argument("--oracle-1thread", action="store_true", help=argparse.SUPPRESS)
     args = ap.parse_args()
     args.warmup = max(3, args.warmup)
@@ -660,8 +660,18 @@ def main():
     wl = Workload(args.config, rank, world, layers=args.layers or None)
     NT = wl.layers
     comms = []
+    ar_note = None
+    if args.ar is None:
+        args.ar = "fused" if world > 1 else "nccl"
     if args.ar == "fused":
-        wl.set_fused_allreduce(rank, world)
+        try:
+            wl.set_fused_allreduce(rank, world)
+        except Exception as e:   # e.g. CUDA IPC not permitted: fall back to the NCCL path, say so
+            if world == 1:
+                raise
+            ar_note = f"fused all-reduce unavailable ({type(e).__name__}: {e}); NCCL used"
+            args.ar = "nccl"
+            wl.ar_peers = {}
     if world > 1:
         if args.ar == "nccl":
             # one NCCL communicator per side; libmux enqueues each layer's all-reduce of the out-proj
@@ -967,7 +977,8 @@ def main():
                    "tbt_slo_ms": args.tbt_slo_ms, "tbt_ms": t_step * 1e3 * NT / D,
                    "decode_num_splits": ns, "parallelism": f"kv-head shard x{world}" if world > 1 else "single GPU",
                    "allreduce": ("fused out-proj GEMM + all-reduce kernel (peer memory)" if args.ar == "fused"
-                                 else "NCCL all-reduce per layer" if world > 1 else "none (one rank)"),
+                                 else "NCCL all-reduce per layer" if world > 1 else "none (one rank)")
+                                + (f"; {ar_note}" if ar_note else ""),
                    "l2": ("L2 flushed (256 MB write) before every timed step" if flush is not None else
                           "inputs larger than L2 (KV pool of every layer >> 126 MB; layers rotate)")},
         "roofline": roofline, "roofline_decode": roofline_dec,

@@ -175,3 +175,75 @@ def test_collective_order_identical_across_ranks():
     pf, dc = allp[0][("pf", 0)], allp[0][("dc", 1)]
     assert [l for l, _ in pf] == list(range(80)) and all(n == 8192 * 8192 for _, n in pf)
     assert [l for l, _ in dc] == [(37 + i) % 80 for i in range(37)] and all(n == 64 * 8192 for _, n in dc)
+
+
+def _peerset_worker(rank, world, port, q):
+    """nccl.PeerSet over gloo with a host-only stand-in for the CUDA IPC buffers: every rank must
+    end up with the same per-rank address table, its own buffers at its own index and every other
+    rank's buffers opened from THAT rank's handles (f4 fused all-reduce peers)."""
+    import torch.distributed as dist
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from paper_2504_14489_b200 import binding, nccl
+
+        class FakeIpc:
+            made = 0
+
+            def __init__(self, nbytes=0, handle=None):
+                if handle is None:
+                    FakeIpc.made += 1
+                    self.handle = f"r{rank}b{FakeIpc.made}".encode().ljust(64, b"\0")
+                    self.owner = rank
+                else:
+                    self.handle, self.owner = handle, int(handle[1:2])
+                self.nbytes = nbytes
+
+            @classmethod
+            def open(cls, handle, nbytes):
+                return cls(nbytes, handle)
+
+            @property
+            def address(self):   # a stand-in "mapped address": the allocation's identity
+                return int.from_bytes(self.handle.rstrip(b"\0")[-2:], "little") + (self.owner << 32)
+
+            def tensor(self, shape, dtype):
+                return None
+
+            def close(self):
+                pass
+
+        binding.IpcBuffer = FakeIpc
+        binding.mux_outproj_ar_ws_bytes = lambda T, N, G: 4096
+        import paper_2504_14489_b200.binding as b2
+        assert b2.IpcBuffer is FakeIpc
+        ps = nccl.PeerSet(rank, world, 300, 264)
+        rk, epoch, stages, ys = ps.peers()
+        owners = [a >> 32 for a in stages] + [a >> 32 for a in ys]
+        q.put((rank, rk, epoch, owners, stages, ys))
+    except Exception as e:  # pragma: no cover
+        q.put((rank, repr(e)))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_peer_set_exchange_gloo():
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    world = 3
+    ps = [ctx.Process(target=_peerset_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in ps:
+        p.start()
+    res = {}
+    for _ in ps:
+        item = q.get(timeout=120)
+        res[item[0]] = item
+    for p in ps:
+        p.join(timeout=60)
+    for r in range(world):
+        assert len(res[r]) == 6, res[r]
+        _, rk, epoch, owners, stages, ys = res[r]
+        assert rk == r and epoch == 0
+        assert owners == list(range(world)) * 2            # slot r holds rank r's buffers
+        assert stages == res[0][4] and ys == res[0][5]      # the same table on every rank
