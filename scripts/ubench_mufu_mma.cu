@@ -91,6 +91,43 @@ __global__ void __launch_bounds__(544, 1) kern(long long* out, int iters, int mo
           while (clock64() - t < 1500) __nanosleep(100);
         }
       }
+    } else if (mode == 11 || mode == 12) {   // TMEM loads as ONE 64-column op (11) / 16x256b shape (12)
+      while (!done) {
+        uint32_t r[64];
+        if (mode == 11) {
+          asm volatile(
+              "tcgen05.ld.sync.aligned.32x32b.x64.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+              "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31,%32,%33,%34,%35,%36,%37,%38,%39,"
+              "%40,%41,%42,%43,%44,%45,%46,%47,%48,%49,%50,%51,%52,%53,%54,%55,%56,%57,%58,%59,%60,%61,%62,%63}, [%64];"
+              : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+                "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15]),
+                "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]),
+                "=r"(r[24]), "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31]),
+                "=r"(r[32]), "=r"(r[33]), "=r"(r[34]), "=r"(r[35]), "=r"(r[36]), "=r"(r[37]), "=r"(r[38]), "=r"(r[39]),
+                "=r"(r[40]), "=r"(r[41]), "=r"(r[42]), "=r"(r[43]), "=r"(r[44]), "=r"(r[45]), "=r"(r[46]), "=r"(r[47]),
+                "=r"(r[48]), "=r"(r[49]), "=r"(r[50]), "=r"(r[51]), "=r"(r[52]), "=r"(r[53]), "=r"(r[54]), "=r"(r[55]),
+                "=r"(r[56]), "=r"(r[57]), "=r"(r[58]), "=r"(r[59]), "=r"(r[60]), "=r"(r[61]), "=r"(r[62]), "=r"(r[63])
+              : "r"(lane_off + (warp & 1) * 64));
+        } else {
+          // 16 lanes x 256 bits twice: same bytes, other lane mapping
+#pragma unroll
+          for (int h = 0; h < 2; ++h)
+            asm volatile(
+                "tcgen05.ld.sync.aligned.16x256b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+                "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+                : "=r"(r[32 * h + 0]), "=r"(r[32 * h + 1]), "=r"(r[32 * h + 2]), "=r"(r[32 * h + 3]), "=r"(r[32 * h + 4]),
+                  "=r"(r[32 * h + 5]), "=r"(r[32 * h + 6]), "=r"(r[32 * h + 7]), "=r"(r[32 * h + 8]), "=r"(r[32 * h + 9]),
+                  "=r"(r[32 * h + 10]), "=r"(r[32 * h + 11]), "=r"(r[32 * h + 12]), "=r"(r[32 * h + 13]),
+                  "=r"(r[32 * h + 14]), "=r"(r[32 * h + 15]), "=r"(r[32 * h + 16]), "=r"(r[32 * h + 17]),
+                  "=r"(r[32 * h + 18]), "=r"(r[32 * h + 19]), "=r"(r[32 * h + 20]), "=r"(r[32 * h + 21]),
+                  "=r"(r[32 * h + 22]), "=r"(r[32 * h + 23]), "=r"(r[32 * h + 24]), "=r"(r[32 * h + 25]),
+                  "=r"(r[32 * h + 26]), "=r"(r[32 * h + 27]), "=r"(r[32 * h + 28]), "=r"(r[32 * h + 29]),
+                  "=r"(r[32 * h + 30]), "=r"(r[32 * h + 31])
+                : "r"(lane_off + (warp & 1) * 64 + h * 32));
+        }
+        dev::tmem_wait_ld();
+        acc += __uint_as_float(r[0] ^ r[63]);
+      }
     } else if (mode == 8) {   // row max over registers only
       uint32_t r[64];
 #pragma unroll
@@ -151,10 +188,10 @@ int main() {
   const char* names[] = {"exp warps alone", "+ MMA QK(SS)+PV(TS)", "+ MMA QK(SS) only", "+ MMA PV(TS) only",
                          "+ 2 warps/SMSP LDTM+max", "+ 2 warps/SMSP mbar sleep", "+ 2 warps/SMSP exp mix",
                          "+ 2 warps/SMSP LDTM only", "+ 2 warps/SMSP FMNMX only", "+ 2 warps/SMSP STTM only",
-                         "+ LDTM every ~1500 cyc"};
+                         "+ LDTM every ~1500 cyc", "+ LDTM as one x64 op", "+ LDTM 16x256b x8 x2"};
   const int iters = 200;
   for (int rep = 0; rep < 2; ++rep)
-    for (int mode = 0; mode < 11; ++mode) {
+    for (int mode = 0; mode < 12; ++mode) {
       cudaMemset(d, 0, 64);
       kern<<<148, 544, 100 * 1024>>>(d, iters, mode);
       cudaError_t e = cudaDeviceSynchronize();
