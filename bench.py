@@ -752,9 +752,16 @@ def main():
         measure_mux(e)
     # the paper's serving objective is goodput under SLOs: the split must keep a decode token's
     # time between tokens (an iteration = N_T layers = N_T / D steps) within the TBT SLO
-    ok = [e for e in sweep if e["tbt_ms"] <= args.tbt_slo_ms] or sweep
+    # (3 % margin: the timed steps run a little slower than the calibration's three)
+    ok = ([e for e in sweep if e["tbt_ms"] <= 0.97 * args.tbt_slo_ms] or
+          [e for e in sweep if e["tbt_ms"] <= args.tbt_slo_ms] or sweep)
+    # bubble-less: only splits whose two sides are busy for all but <= 5 % of the window
+    # on average (the idle share of the shorter side, halved); the fastest of those
+    for e in sweep:
+        e["bubble_pred"] = 0.5 * abs(e["dec_side_ms"] - e["pf_side_ms"]) / max(e["dec_side_ms"], e["pf_side_ms"])
+    ok = [e for e in ok if e["bubble_pred"] <= 0.05] or ok
     best = max(ok, key=lambda e: e["tok_s"])
-    # bubble-less: among candidates within 1 % of the best rate, the most balanced sides
+    # among candidates within 1 % of the best rate, the most balanced sides
     near = [e for e in ok if e["tok_s"] >= 0.99 * best["tok_s"]]
     best = min(near, key=lambda e: abs(e["dec_side_ms"] - e["pf_side_ms"]) / max(e["dec_side_ms"], e["pf_side_ms"]))
     if world > 1:  # every rank must run the same split: rank 0 decides
