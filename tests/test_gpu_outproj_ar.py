@@ -138,3 +138,38 @@ def test_fused_allreduce_rejects_bad_args(mux):
     y = torch.empty((256, 64), dtype=torch.bfloat16, device="cuda")
     with pytest.raises(mux.MuxError):
         mux.mux_outproj_allreduce(x, w, 1, 1, [st], [y])          # rank outside the world
+
+
+def test_fused_allreduce_cfg4_full_size(mux):
+    """BASELINE cfg4 (Llama-3-70B, KV-head sharded over 8 GPUs, P:686 / P:701-702): each rank's
+    out-projection of the 8192-token prefill, X [8192][Hq/8 * 128 = 1024] . W_o shard [1024][8192],
+    all-reduced over 8 emulated ranks.  Every rank's Y is bitwise the composition (bf16 GEMM partials
+    summed in rank order); 64 rows spread over the tiles (first / last row, tile boundaries) match the
+    float64 unsharded product within the wire-type bound."""
+    import torch
+    G, T, K, N = 8, 8192, 1024, 8192
+    g = synth.rng(4, synth.T_WO, salt=88)
+    xs = [torch.from_numpy(synth.bf16_normal(g, (T, K)).view(np.int16)).cuda().view(torch.bfloat16) for _ in range(G)]
+    ws_h = [synth.bf16_normal(g, (K, N), std=1 / math.sqrt(G * K)) for _ in range(G)]
+    ws = [mux.mux_outproj_pack_w(_dev(w)) for w in ws_h]
+    wsb = mux.mux_outproj_ar_ws_bytes(T, N, G)
+    stages = [torch.zeros(wsb, dtype=torch.uint8, device="cuda") for _ in range(G)]
+    ys = [torch.empty((T, N), dtype=torch.bfloat16, device="cuda") for _ in range(G)]
+    mux.mux_outproj_allreduce_emulated(xs, ws, 0, stages, ys)
+    acc = None
+    for r in range(G):
+        p = torch.empty((T, N), dtype=torch.bfloat16, device="cuda")
+        mux.mux_outproj(xs[r], ws[r], p)
+        acc = p.float() if acc is None else acc + p.float()
+    torch.cuda.synchronize()
+    comp = acc.bfloat16().view(torch.int16)
+    for r in range(G):
+        assert torch.equal(ys[r].view(torch.int16), comp), f"rank {r}"
+    rows = synth.sample_rows(T, 64, tile=256)
+    idx = torch.from_numpy(rows.astype(np.int64)).cuda()
+    xs_h = [x[idx].view(torch.int16).cpu().numpy().view(np.uint16) for x in xs]
+    ref = oracle.outproj(np.concatenate(xs_h, axis=1), np.concatenate(ws_h, axis=0))
+    parts = [oracle.outproj(xs_h[r], ws_h[r]) for r in range(G)]
+    bound = 2.0 ** -8 * (sum(np.abs(p) for p in parts) + np.abs(ref)) + 1e-4
+    d = np.abs(_f64(ys[3][idx]) - ref)
+    assert (d <= bound).all(), f"max|d| {d.max():.3e}"
