@@ -6,6 +6,7 @@
 #include "../paper_2504_14489_b200/csrc/mux_internal.h"
 using namespace mux;
 
+template <int EMU = 0>   // EMU of every 8 pairs take exp2 on the FMA pipe (dev::ex2_poly_pair)
 __device__ __forceinline__ float exp_mix(uint32_t (&s)[64], float sl2, float neg_m) {
   const uint64_t S2 = dev::f2pack(sl2, sl2), OF = dev::f2pack(neg_m, neg_m);
   uint64_t acc = dev::f2pack(0.f, 0.f);
@@ -13,7 +14,13 @@ __device__ __forceinline__ float exp_mix(uint32_t (&s)[64], float sl2, float neg
   for (int i = 0; i < 32; ++i) {
     float a, b;
     dev::f2unpack(dev::ffma2(dev::f2pack(__uint_as_float(s[2 * i]), __uint_as_float(s[2 * i + 1])), S2, OF), a, b);
-    const float e0 = dev::ex2(a), e1 = dev::ex2(b);
+    float e0, e1;
+    if ((i & 7) < EMU) {
+      dev::ex2_poly_pair(a, b, e0, e1);
+    } else {
+      e0 = dev::ex2(a);
+      e1 = dev::ex2(b);
+    }
     acc = dev::fadd2(acc, dev::f2pack(e0, e1));
     const uint32_t pk = dev::pack_f16(e0, e1);
     s[2 * i] ^= pk & 1u;
@@ -24,6 +31,7 @@ __device__ __forceinline__ float exp_mix(uint32_t (&s)[64], float sl2, float neg
   return a0 + a1;
 }
 
+template <int EMU>
 __global__ void __launch_bounds__(544, 1) kern(long long* out, int iters, int mode) {
   extern __shared__ __align__(1024) uint8_t sm[];
   __shared__ uint64_t bar;
@@ -165,7 +173,7 @@ __global__ void __launch_bounds__(544, 1) kern(long long* out, int iters, int mo
     float acc = 0.f;
     __syncwarp();
     long long t0 = clock64();
-    for (int it = 0; it < iters; ++it) acc += exp_mix(v, 1.4426950f, -0.5f);
+    for (int it = 0; it < iters; ++it) acc += exp_mix<EMU>(v, 1.4426950f, -0.5f);
     long long t1 = clock64();
     if (acc == 12345.f) out[3] = 1;
     if (blockIdx.x == 0 && warp == 1 && (threadIdx.x & 31) == 0) out[0] = t1 - t0;
@@ -184,21 +192,26 @@ int main() {
   long long* d;
   cudaMalloc(&d, 64);
   long long h[4];
-  cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 100 * 1024);
   const char* names[] = {"exp warps alone", "+ MMA QK(SS)+PV(TS)", "+ MMA QK(SS) only", "+ MMA PV(TS) only",
                          "+ 2 warps/SMSP LDTM+max", "+ 2 warps/SMSP mbar sleep", "+ 2 warps/SMSP exp mix",
                          "+ 2 warps/SMSP LDTM only", "+ 2 warps/SMSP FMNMX only", "+ 2 warps/SMSP STTM only",
-                         "+ LDTM every ~1500 cyc", "+ LDTM as one x64 op", "+ LDTM 16x256b x8 x2"};
+                         "+ LDTM every ~1500 cyc", "+ LDTM as one x64 op"};
   const int iters = 200;
-  for (int rep = 0; rep < 2; ++rep)
-    for (int mode = 0; mode < 12; ++mode) {
-      cudaMemset(d, 0, 64);
-      kern<<<148, 544, 100 * 1024>>>(d, iters, mode);
-      cudaError_t e = cudaDeviceSynchronize();
-      cudaMemcpy(h, d, 32, cudaMemcpyDeviceToHost);
-      // per iteration: 2 warps per SMSP x 64 ex2 -> MUFU floor 2 * 64 * 8 = 1024 cycles
-      printf("%-24s %s: %.0f cycles per 64-element iteration (2 warps/SMSP; MUFU floor 1024), mma patterns %lld\n",
-             names[mode], cudaGetErrorString(e), double(h[0]) / iters, h[2]);
-    }
+  auto run = [&](auto kfn, int emu, int mode) {
+    cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, 100 * 1024);
+    cudaMemset(d, 0, 64);
+    kfn<<<148, 544, 100 * 1024>>>(d, iters, mode);
+    cudaError_t e = cudaDeviceSynchronize();
+    cudaMemcpy(h, d, 32, cudaMemcpyDeviceToHost);
+    printf("emu %d/8  %-24s %s: %.0f cycles per 64-element iteration (MUFU-only floor 1024)\n", emu, names[mode],
+           cudaGetErrorString(e), double(h[0]) / iters);
+  };
+  const int modes_all[] = {0, 1, 2, 3, 4, 5, 6, 7, 8, 9, 10, 11};
+  const int modes_emu[] = {0, 4, 10, 7};
+  for (int m : modes_all) run(kern<0>, 0, m);
+  for (int m : modes_emu) run(kern<1>, 1, m);
+  for (int m : modes_emu) run(kern<2>, 2, m);
+  for (int m : modes_emu) run(kern<3>, 3, m);
+  for (int m : modes_emu) run(kern<4>, 4, m);
   return 0;
 }
