@@ -666,8 +666,8 @@ def main():
     if args.ar == "fused":
         try:
             wl.set_fused_allreduce(rank, world)
-        except Exception as e:   # e.g. CUDA IPC not permitted: fall back to the NCCL path, say so
-            if world == 1:
+        except Exception as e:   # e.g. no CUDA IPC / peer access: every rank falls back together (PeerSet
+            if world == 1:       # agrees on failures collectively) to the NCCL path, and says so
                 raise
             ar_note = f"fused all-reduce unavailable ({type(e).__name__}: {e}); NCCL used"
             args.ar = "nccl"

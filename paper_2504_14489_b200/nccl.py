@@ -115,23 +115,46 @@ class PeerSet:
         self.rank, self.world, self.T, self.N = rank, world, T, N
         ws_bytes = mux_outproj_ar_ws_bytes(T, N, world)
         y_bytes = T * N * 2
-        self.mine = [IpcBuffer(ws_bytes), IpcBuffer(y_bytes)]
-        handles = [(self.mine[0].handle, self.mine[1].handle)]
+        self.mine, self.opened = [], []
+        self.stage_addr, self.y_addr, self.y_bufs = [], [], []
+
+        def agree(ok: bool, err):
+            # every rank reaches every exchange, so a failure on one rank fails all of them together
+            # (a rank that raised alone would leave the others blocked in the next collective)
+            if world == 1:
+                if not ok:
+                    raise err
+                return
+            flags = [None] * world
+            dist.all_gather_object(flags, ok)
+            if not all(flags):
+                self.close()
+                raise RuntimeError(f"PeerSet: ranks {[r for r, f in enumerate(flags) if not f]} failed: {err!r}")
+
+        err = None
+        try:
+            self.mine = [IpcBuffer(ws_bytes), IpcBuffer(y_bytes)]
+            handles = [(self.mine[0].handle, self.mine[1].handle)]
+        except Exception as e:
+            err, handles = e, [None]
         if world > 1:
             allh = [None] * world
             dist.all_gather_object(allh, handles[0])
             handles = allh
-        self.opened = []
-        self.stage_addr, self.y_addr, self.y_bufs = [], [], []
-        for r in range(world):
-            if r == rank:
-                st, y = self.mine
-            else:
-                st, y = IpcBuffer.open(handles[r][0], ws_bytes), IpcBuffer.open(handles[r][1], y_bytes)
-                self.opened += [st, y]
-            self.stage_addr.append(st.address)
-            self.y_addr.append(y.address)
-            self.y_bufs.append(y)
+        agree(err is None and all(h is not None for h in handles), err)
+        try:
+            for r in range(world):
+                if r == rank:
+                    st, y = self.mine
+                else:
+                    st, y = IpcBuffer.open(handles[r][0], ws_bytes), IpcBuffer.open(handles[r][1], y_bytes)
+                    self.opened += [st, y]
+                self.stage_addr.append(st.address)
+                self.y_addr.append(y.address)
+                self.y_bufs.append(y)
+        except Exception as e:
+            err = e
+        agree(err is None, err)
         self.y = self.mine[1].tensor((T, N), torch.bfloat16)   # this rank's reduced output
 
     def peers(self):

@@ -177,7 +177,7 @@ def test_collective_order_identical_across_ranks():
     assert [l for l, _ in dc] == [(37 + i) % 80 for i in range(37)] and all(n == 64 * 8192 for _, n in dc)
 
 
-def _peerset_worker(rank, world, port, q):
+def _peerset_worker(rank, world, port, q, fail_open_on=-1):
     """nccl.PeerSet over gloo with a host-only stand-in for the CUDA IPC buffers: every rank must
     end up with the same per-rank address table, its own buffers at its own index and every other
     rank's buffers opened from THAT rank's handles (f4 fused all-reduce peers)."""
@@ -201,6 +201,8 @@ def _peerset_worker(rank, world, port, q):
 
             @classmethod
             def open(cls, handle, nbytes):
+                if rank == fail_open_on:
+                    raise OSError("peer access refused (test)")
                 return cls(nbytes, handle)
 
             @property
@@ -217,7 +219,11 @@ def _peerset_worker(rank, world, port, q):
         binding.mux_outproj_ar_ws_bytes = lambda T, N, G: 4096
         import paper_2504_14489_b200.binding as b2
         assert b2.IpcBuffer is FakeIpc
-        ps = nccl.PeerSet(rank, world, 300, 264)
+        try:
+            ps = nccl.PeerSet(rank, world, 300, 264)
+        except RuntimeError as e:
+            q.put((rank, "raised", str(e)))
+            return
         rk, epoch, stages, ys = ps.peers()
         owners = [a >> 32 for a in stages] + [a >> 32 for a in ys]
         q.put((rank, rk, epoch, owners, stages, ys))
@@ -247,3 +253,23 @@ def test_peer_set_exchange_gloo():
         assert rk == r and epoch == 0
         assert owners == list(range(world)) * 2            # slot r holds rank r's buffers
         assert stages == res[0][4] and ys == res[0][5]      # the same table on every rank
+
+
+def test_peer_set_failure_is_collective_gloo():
+    """one rank cannot map its peers: every rank raises (none is left blocked in a collective), so
+    bench.py falls back to NCCL on all ranks together"""
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    world = 3
+    ps = [ctx.Process(target=_peerset_worker, args=(r, world, port, q, 1)) for r in range(world)]
+    for p in ps:
+        p.start()
+    res = {}
+    for _ in ps:
+        item = q.get(timeout=120)
+        res[item[0]] = item
+    for p in ps:
+        p.join(timeout=60)
+    for r in range(world):
+        assert res[r][1] == "raised" and "ranks [1] failed" in res[r][2], res[r]
