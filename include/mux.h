@@ -342,7 +342,9 @@ int mux_outproj_sms(const void* x, const void* w_packed, void* y, int32_t y_dtyp
  * first call) and its Y, as addresses valid in THIS process (peers' allocations mapped by CUDA
  * IPC or VMM; rank == r: local).  Every rank calls with the same T, K, N, world and epoch.
  * num_sms: SMs the launch may use (<= 0: the device); one CTA per SM, so all of a rank's CTAs are
- * resident and the cross-rank waits cannot deadlock.  Any T >= 1 (a decode side's few rows run in
+ * resident and the cross-rank waits cannot deadlock; a rank that never arrives (crashed peer,
+ * mismatched calls) makes the waiting kernels trap after 20 s instead of hanging the GPU (the
+ * launch then fails with a CUDA error).  Any T >= 1 (a decode side's few rows run in
  * one 256-row tile; rows past T are zero-filled and never stored).  Requirements: K and N multiples
  * of 8, 16-byte aligned buffers.  Errors: MUX_ERR_INVALID_ARG / MUX_ERR_UNSUPPORTED / MUX_ERR_CUDA. */
 #define MUX_AR_MAX_WORLD 8

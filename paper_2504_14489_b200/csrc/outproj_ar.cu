@@ -78,8 +78,18 @@ __device__ __forceinline__ uint32_t ld_acquire_sys(const uint32_t* a) {
   return v;
 }
 __device__ __forceinline__ void fence_sys() { asm volatile("fence.acq_rel.sys;" ::: "memory"); }
+// A rank that never arrives (a peer that crashed, or ranks that called with different arguments)
+// must not hang the GPU: after kArWaitLimitNs the kernel traps (the launch fails with an error).
+#ifndef MUX_AR_WAIT_LIMIT_NS
+#define MUX_AR_WAIT_LIMIT_NS 20000000000ull
+#endif
 __device__ __forceinline__ void wait_count(const uint32_t* a, uint32_t target) {
-  while (static_cast<int32_t>(ld_acquire_sys(a) - target) < 0) __nanosleep(64);
+  if (static_cast<int32_t>(ld_acquire_sys(a) - target) >= 0) return;
+  const uint64_t t0 = dev::globaltimer();
+  while (static_cast<int32_t>(ld_acquire_sys(a) - target) < 0) {
+    __nanosleep(64);
+    if (dev::globaltimer() - t0 > MUX_AR_WAIT_LIMIT_NS) __trap();
+  }
 }
 
 __global__ void __launch_bounds__(kArThreads, 1)
