@@ -339,7 +339,8 @@ int mux_outproj_sms(const void* x, const void* w_packed, void* y, int32_t y_dtyp
  * the host; else an explicit counter shared by all ranks, 1 on the first call with a workspace, +1
  * per call; the two modes must not be mixed on one workspace; counters are never reset) and, per rank r,
  * its staging workspace (mux_outproj_ar_ws_bytes(T, N, G) bytes, zero-filled ONCE before the
- * first call) and its Y, as addresses valid in THIS process (peers' allocations mapped by CUDA
+ * first call; a workspace serves one (T, N, G): its counters sit behind T x N-sized slots) and its Y,
+ * as addresses valid in THIS process (peers' allocations mapped by CUDA
  * IPC or VMM; rank == r: local).  Every rank calls with the same T, K, N, world and epoch.
  * num_sms: SMs the launch may use (<= 0: the device); one CTA per SM, so all of a rank's CTAs are
  * resident and the cross-rank waits cannot deadlock; a rank that never arrives (crashed peer,
