@@ -280,3 +280,44 @@ def test_run_layer_fused_allreduce_side(mux, part):
                 assert torch.equal(y.view(torch.int16), y2.view(torch.int16)), f"split {split}"
             else:   # same fp32 products, another MMA shape: within one bf16 rounding
                 assert ((y.float() - y2.float()).abs() <= 2.0 ** -8 * y2.float().abs() + 1e-3).all(), f"split {split}"
+
+
+def test_run_layer_fused_allreduce_multi_layer(mux, part):
+    """f4 over a side of 2 layers with per-layer o / y (y_stride): each layer's out-projection +
+    all-reduce is its own fused launch on automatic epochs (three consecutive mux_run_layer calls
+    on one workspace); every layer's y is bitwise the standalone out-projection of that layer's o."""
+    import torch
+    import synth
+    from synth import indptr
+    Hq, Hkv, d, hidden = 4, 1, 64, 256
+    pf = make_side(804, Shapes(Hq, Hkv, d, 1), SideSpec([64], [200]), decode=False)
+    need = sum(pf.spec.pages_needed())
+    kst = torch.full((2, need + 4, Hkv, 16, d), 0x7FC0, dtype=torch.int16, device="cuda").view(torch.bfloat16)
+    pool = mux.Pool(2, need + 4, Hkv, d, 9, kst, kst.clone())
+    pind, pids = pool.page_tables(pf.spec.pages_needed())
+    pre = mux.Batch(indptr(pf.spec.r), pf.spec.r, [0, 4], pids[:4])
+    kpre = torch.from_numpy(pf.k_cached().view(np.int16)).cuda().view(torch.bfloat16)
+    vpre = torch.from_numpy(pf.v_cached().view(np.int16)).cuda().view(torch.bfloat16)
+    for layer in (0, 1):
+        mux.mux_append_kv(pool, layer, pre, kpre, vpre)
+    batch = mux.Batch(indptr(pf.spec.n), pf.spec.L, pind, pids)
+    T = pf.spec.total_new
+    q = torch.from_numpy(np.stack([pf.q, pf.q]).view(np.int16)).cuda().view(torch.bfloat16)
+    kn = torch.from_numpy(np.stack([pf.k_new(), pf.k_new()]).view(np.int16)).cuda().view(torch.bfloat16)
+    vn = torch.from_numpy(np.stack([pf.v_new(), pf.v_new()]).view(np.int16)).cuda().view(torch.bfloat16)
+    wo_bits = synth.make_wo(805, Shapes(Hq, Hkv, d, 1, hidden=hidden))
+    w_o = mux.mux_outproj_pack_w(torch.from_numpy(wo_bits.view(np.int16)).cuda().view(torch.bfloat16))
+    stage = torch.zeros(mux.mux_outproj_ar_ws_bytes(T, hidden, 1), dtype=torch.uint8, device="cuda")
+    for call in range(3):
+        o = torch.zeros((2, T, Hq, d), dtype=torch.bfloat16, device="cuda")
+        y = torch.full((2, T, hidden), float("nan"), dtype=torch.bfloat16, device="cuda")
+        s = mux.make_side(batch, Hq, q, o, k_new=kn, v_new=vn, scale=0.125, num_layers=2, append=True,
+                          per_layer_inputs=True, w_o=w_o, y=y, ar_peers=(0, 0, [stage], [y]))
+        mux.mux_run_layer(part, 1 if call % 2 else -1, pool, s, None, None)
+        torch.cuda.synchronize()
+        for layer in (0, 1):
+            y2 = torch.empty((T, hidden), dtype=torch.bfloat16, device="cuda")
+            mux.mux_outproj(o[layer].view(T, -1), w_o, y2)
+            torch.cuda.synchronize()
+            assert not torch.isnan(y[layer].float()).any(), f"call {call} layer {layer}"
+            assert torch.equal(y[layer].view(torch.int16), y2.view(torch.int16)), f"call {call} layer {layer}"
