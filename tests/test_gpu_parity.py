@@ -128,6 +128,12 @@ PREFILL_CASES = [
     (128, 6, 2, [0, 50, 16], [140, 77, 1]),           # g = 3 d128: prefill_kernel<128, 1>
     (64, 6, 2, [20], [150]),                          # g = 3 d64: prefill_kernel<64, 1>
     (128, 12, 6, [17], [130]),                        # Hkv = 6, g = 2 (head pairs)
+    # v6 cluster (multicast K/V, g % 4 == 0) with the K-first / adaptive producer order: one tile, one row
+    (128, 8, 2, [0], [1]),
+    (128, 8, 2, [16], [16]),                          # one cached page + one new page: nt = 1
+    (128, 16, 4, [0, 4096, 33, 511], [1, 257, 640, 2]),   # 4 ragged sequences, 1..33 key tiles
+    (128, 32, 8, [8191], [2]),                        # Llama-3-8B heads, 65 key tiles, one partial q tile
+    (128, 4, 1, [256], [256]),                        # prefix and rows on 128-key tile boundaries
 ]
 
 
