@@ -151,3 +151,22 @@ def test_version_and_error_string(mux):
     with pytest.raises(mux.MuxError):
         _fake_pool(mux, 8, 1, d=96)
     assert "head_dim" in mux.last_error()
+
+
+def test_header_is_plain_c_and_cxx(tmp_path):
+    """include/mux.h is a C ABI: it must compile as strict C99 and as C++11 (no torch or C++-only
+    types), including the structs a caller fills (mux_side, mux_ar_peers, mux_batch)."""
+    import shutil
+    import subprocess
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    src = ("#include \"mux.h\"\n"
+           "int main(void) { mux_side s; mux_ar_peers p; mux_batch b; (void)s; (void)p; (void)b;\n"
+           "  return mux_outproj_ar_ws_bytes(256, 256, 2) == 0; }\n")
+    for comp, std, ext in (("gcc", "-std=c99", "c"), ("g++", "-std=c++11", "cpp")):
+        if not shutil.which(comp):
+            pytest.skip(f"{comp} not found")
+        f = tmp_path / f"t.{ext}"
+        f.write_text(src)
+        r = subprocess.run([comp, std, "-Wall", "-Wextra", "-pedantic", "-Werror", "-fsyntax-only",
+                            "-I", os.path.join(root, "include"), str(f)], capture_output=True, text=True)
+        assert r.returncode == 0, r.stderr
