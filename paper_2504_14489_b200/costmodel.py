@@ -60,12 +60,16 @@ def _list_makespan(durations, k: int) -> float:
 
 def prefill_wave_features(r: Sequence[int], n: Sequence[int], sms: int, hq: int = 32, hkv: int = 8, d: int = 128,
                           cta_overhead_tiles: float = 3.0) -> np.ndarray:
-    """[attention makespan (128-key tile units), out-projection waves, sum n, 1] of one layer on
-    `sms` SMs: the prefill grid (q tile x head pair x sequence, csrc/prefill.cu tile_coord order:
-    q tiles longest-first grid-wide when the batch K/V is <= 64 MB, else per sequence heavy-first)
-    and the CTA-pair out-projection GEMM (256 x 256 tiles of T x hidden over sms/2 pairs).  A CTA
-    costs its key tiles + ~3 tiles of prologue / epilogue (TMEM alloc, Q load, O write), the
-    constant that fits the recorded B200 samples best (profiles/r02_costmodel.json)."""
+    """[attention makespan (128-key tile units), out-projection waves, sum n, 1, K/V MB streamed
+    from HBM] of one layer on `sms` SMs: the prefill grid (q tile x head pair x sequence,
+    csrc/prefill.cu tile_coord order: q tiles longest-first grid-wide when the batch K/V is <= 64 MB,
+    else per sequence heavy-first) and the CTA-pair out-projection GEMM (256 x 256 tiles of T x
+    hidden over sms/2 pairs).  A CTA costs its key tiles + ~3 tiles of prologue / epilogue (TMEM
+    alloc, Q load, O write), the constant that fits the recorded B200 samples best
+    (profiles/r02_costmodel.json).  The last term is the batch's K/V in MB when it exceeds the L2
+    budget (> 64 MB, the per-sequence order): the K/V then comes from HBM rather than L2, which the
+    tile makespan alone does not see (two 1k chunks on 8k prefixes ran 11 % above the 4-term fit on
+    148 SMs, profiles/r02q_costmodel.json; with the term <= 9.5 % on every partition)."""
     keys = sum(a + b for a, b in zip(r, n))
     nq = max((x + 127) // 128 for x in n)
     heads = max(1, hq // 2)
@@ -83,7 +87,9 @@ def prefill_wave_features(r: Sequence[int], n: Sequence[int], sms: int, hq: int 
                 ctas += [cta(b, qi) for qi in range((n[b] + 127) // 128 - 1, -1, -1)]
     T = sum(n)
     waves = math.ceil(math.ceil(T / 256) * 16 / max(1, sms // 2))
-    return np.array([_list_makespan(ctas, sms), float(waves), float(T), 1.0])
+    kv_bytes = keys * hkv * 4 * d
+    kv_hbm_mb = kv_bytes / 1e6 if kv_bytes > 64 * 2 ** 20 else 0.0
+    return np.array([_list_makespan(ctas, sms), float(waves), float(T), 1.0, kv_hbm_mb])
 
 
 def decode_wave_features(r: Sequence[int], sms: int, hkv: int = 8, d: int = 128, num_splits: int = 0,
