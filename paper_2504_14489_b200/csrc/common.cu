@@ -56,6 +56,7 @@ int driver(const Driver** out) {
     ok &= entry("cuGreenCtxStreamCreate", &d.greenCtxStreamCreate);
     ok &= entry("cuGreenCtxGetDevResource", &d.greenCtxGetDevResource);
     ok &= entry("cuStreamDestroy", &d.streamDestroy);
+    entry("cuStreamGetGreenCtx", &d.streamGetGreenCtx);
     d.ok = ok;
   });
   if (!d.ok) return fail(MUX_ERR_CUDA, "CUDA driver entry points unavailable (no driver / GPU?)");
@@ -90,6 +91,18 @@ int device_sm_count() {
   int dev = current_device(), n = 0;
   if (cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess) return 0;
   return n;
+}
+
+int stream_sm_count(cudaStream_t stream) {
+  const Driver* d;
+  if (stream && driver(&d) == MUX_OK && d->streamGetGreenCtx) {
+    CUgreenCtx g = nullptr;
+    CUdevResource res{};
+    if (d->streamGetGreenCtx(reinterpret_cast<CUstream>(stream), &g) == CUDA_SUCCESS && g &&
+        d->greenCtxGetDevResource(g, &res, CU_DEV_RESOURCE_TYPE_SM) == CUDA_SUCCESS && res.sm.smCount > 0)
+      return static_cast<int>(res.sm.smCount);
+  }
+  return device_sm_count();
 }
 
 int validate_batch(const mux_batch* b, bool decode_shape) {

@@ -47,6 +47,7 @@ struct Driver {
   decltype(&cuGreenCtxStreamCreate) greenCtxStreamCreate = nullptr;
   decltype(&cuGreenCtxGetDevResource) greenCtxGetDevResource = nullptr;
   decltype(&cuStreamDestroy) streamDestroy = nullptr;
+  decltype(&cuStreamGetGreenCtx) streamGetGreenCtx = nullptr;  // optional (CUDA >= 12.4)
   bool ok = false;
 };
 int driver(const Driver** out);
@@ -57,6 +58,9 @@ int make_tmap_bf16(CUtensorMap* map, const void* base, int rank, const uint64_t*
                    const uint64_t* strides_bytes /* rank-1 entries */, const uint32_t* box, bool swizzle = true);
 
 int device_sm_count();
+// SMs a launch on `stream` can occupy: the SM count of the green context the stream belongs to,
+// else the whole device
+int stream_sm_count(cudaStream_t stream);
 int current_device();
 
 struct PoolImpl;  // pool.cu
@@ -73,6 +77,8 @@ int run_side(mux_pool_t pool, const mux_side* s, bool decode, int sms, cudaStrea
 void launch_stamp(unsigned long long* dst, cudaStream_t st);
 // outproj.cu: mux_outproj with the SM count of the launching partition (persistent grid)
 // a4 decode attention with the launch sized for `num_sms` SMs (the side's partition; <= 0 = device)
+int prefill_launch_sms(mux_pool_t pool, int32_t layer, const mux_batch* b, int32_t hq, const void* q, void* o,
+                       int32_t o_dtype, float* lse, float scale, mux_stream_t stream, int num_sms);
 int decode_launch_sms(mux_pool_t pool, int32_t layer, const mux_batch* b, int32_t hq, const void* q, void* o,
                       int32_t o_dtype, float* lse, float scale, int32_t num_splits, void* ws, size_t ws_bytes,
                       mux_stream_t stream, int num_sms);

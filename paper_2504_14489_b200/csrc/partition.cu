@@ -220,8 +220,8 @@ int run_side(mux_pool_t pool, const mux_side* s, bool decode, int sms, cudaStrea
       rc = decode_launch_sms(pool, layer, s->batch, s->num_q_heads, at(s->q, s->q_stride), o, s->o_dtype, lse,
                              s->scale, splits, s->ws, s->ws_bytes, reinterpret_cast<mux_stream_t>(st), sms);
     else
-      rc = mux_prefill_attn(pool, layer, s->batch, s->num_q_heads, at(s->q, s->q_stride), o, s->o_dtype, lse,
-                            s->scale, reinterpret_cast<mux_stream_t>(st));
+      rc = prefill_launch_sms(pool, layer, s->batch, s->num_q_heads, at(s->q, s->q_stride), o, s->o_dtype, lse,
+                              s->scale, reinterpret_cast<mux_stream_t>(st), sms);
     if (rc) return rc;
     if ((rc = ev(i, 1))) return rc;
     if (s->w_o) {

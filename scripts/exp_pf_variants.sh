@@ -1,4 +1,4 @@
-# prefill A/B: alternating rounds over "name:ENV" pairs (name = libmux_<name>.so; ENV = extra env, "-" none)
+# prefill A/B: alternating rounds over "name:ENV" pairs (name = libmux_<name>.so; ENV = extra env as A=1+B=2, "-" none)
 export PYTHONUNBUFFERED=1
 cd paper_2504_14489_b200; cp libmux.so libmux_keep.so; cd ..
 LOG=gpurun_out/${LOGN:-pf_variants}.log
@@ -9,7 +9,7 @@ for pair in ${PARITY:-}; do
 done
 for r in 1 2 3; do
   for pair in $VARIANTS; do
-    v=${pair%%:*}; e=${pair#*:}; [ "$e" = "-" ] && e=""
+    v=${pair%%:*}; e=${pair#*:}; [ "$e" = "-" ] && e=""; e=${e//+/ }
     cp paper_2504_14489_b200/libmux_$v.so paper_2504_14489_b200/libmux.so
     env $e TAG="$pair r$r" timeout 120 python scripts/pf_perf.py >> $LOG 2>&1
   done

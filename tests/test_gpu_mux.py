@@ -321,3 +321,50 @@ def test_run_layer_fused_allreduce_multi_layer(mux, part):
             torch.cuda.synchronize()
             assert not torch.isnan(y[layer].float()).any(), f"call {call} layer {layer}"
             assert torch.equal(y[layer].view(torch.int16), y2.view(torch.int16)), f"call {call} layer {layer}"
+
+
+def test_prefill_on_partition_stream_sizes_its_grid(mux, part):
+    """mux_prefill_attn called directly on a green-context stream (no SM count in its signature) must
+    size the persistent prefill grid to that context's SMs, exactly as mux_run_layer does with the
+    partition it knows: the cfg2 prefill (one 8k causal sequence, 32 q / 8 kv heads) on the prefill side
+    of the 32-SM decode split gives the same bits both ways, and the direct call is not slower than the
+    run_layer one (a grid sized for the whole device would run two waves of persistent CTAs, ~1.5x)."""
+    import torch
+    from synth import indptr
+    Hq, Hkv, d, L = 32, 8, 128, 8192
+    pages = L // 16 + 4
+    kst = torch.zeros((1, pages, Hkv, 16, d), dtype=torch.bfloat16, device="cuda")
+    pool = mux.Pool(1, pages, Hkv, d, 5, kst, kst.clone())
+    ppi, ppd = pool.page_tables([L // 16])
+    gen = torch.Generator(device="cuda").manual_seed(3)
+    k = torch.randn((L, Hkv, d), generator=gen, device="cuda").bfloat16()
+    v = torch.randn((L, Hkv, d), generator=gen, device="cuda").bfloat16()
+    q = torch.randn((L, Hq, d), generator=gen, device="cuda").bfloat16()
+    batch = mux.Batch(indptr([L]), [L], ppi, ppd)
+    mux.mux_append_kv(pool, 0, batch, k, v)
+    scale = 1 / math.sqrt(d)
+    split = 1                                  # decode 32 SMs / prefill the rest
+    _, psms, _, sp = part.query(split)
+    o_run = torch.empty((L, Hq, d), dtype=torch.bfloat16, device="cuda")
+    o_dir = torch.empty_like(o_run)
+    side = mux.make_side(batch, Hq, q, o_run, scale=scale)
+    st = torch.cuda.ExternalStream(sp)
+    ev = [torch.cuda.Event(enable_timing=True) for _ in range(4)]
+
+    def timed(fn, a, b, stream, reps=5):
+        fn()
+        torch.cuda.synchronize()
+        a.record(stream)
+        for _ in range(reps):
+            fn()
+        b.record(stream)
+        torch.cuda.synchronize()
+        return a.elapsed_time(b) / reps
+
+    cur = torch.cuda.current_stream()
+    t_run = timed(lambda: mux.mux_run_layer(part, split, pool, side, None, None), ev[0], ev[1], cur)
+    t_dir = timed(lambda: mux.mux_prefill_attn(pool, 0, batch, Hq, q, o_dir, None, scale=scale, stream=sp),
+                  ev[2], ev[3], st)
+    assert torch.equal(o_run.view(torch.int16), o_dir.view(torch.int16))
+    assert pool.error_flags() == 0
+    assert t_dir < 1.15 * t_run, f"direct {t_dir:.3f} ms vs run_layer {t_run:.3f} ms on {psms} SMs"
