@@ -283,9 +283,10 @@ def probe_read_bw_contended(mux, part, wl, split, sms, pf_side, nbytes=2 << 30, 
     return got * reps / (a.elapsed_time(b) * 1e-3) / 1e9
 
 
-def time_kernel_alone(mux, part, wl, split, which, reps=5):
+def time_kernel_alone(mux, part, wl, split, which, reps=100, warm=5):
     """Average duration (s) of ONE attention launch (prefill6 / decode kernel of layer 0) on split
-    `split`'s own partition stream, nothing else running, CUDA events on that stream."""
+    `split`'s own partition stream, nothing else running, CUDA events on that stream around `reps`
+    back-to-back launches after `warm` untimed ones; returns (seconds, SM clocks sampled meanwhile)."""
     import torch
     _, _, sd, sp = part.query(split)
     raw = sp if which == "pf" else sd
@@ -301,14 +302,18 @@ def time_kernel_alone(mux, part, wl, split, which, reps=5):
         run = lambda: mux.mux_decode_attn(wl.pool, 0, wl.dc_batch, wl.Hq, wl.dc_q, wl.dc_o, None,  # noqa: E731
                                           scale=wl.scale, num_splits=ns, ws=ws, stream=raw, num_sms=dsms)
     torch.cuda.synchronize()
-    run()
-    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    a.record(st)
-    for _ in range(reps):
+    for _ in range(warm):
         run()
-    b.record(st)
     torch.cuda.synchronize()
-    return a.elapsed_time(b) / reps * 1e-3
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(torch.cuda.current_device()) as clk:
+        a.record(st)
+        for _ in range(reps):
+            run()
+        b.record(st)
+        torch.cuda.synchronize()
+    c = clk.summary()
+    return a.elapsed_time(b) / reps * 1e-3, {"sm_mhz": c.get("sm_mhz"), "reasons": c.get("reasons")}
 
 
 def time_side(mux, part, split, wl, which, dc_layers, reps=3):
@@ -916,7 +921,7 @@ def main():
     bw_part, bw_full = probe_read_bw(mux, part, wl, i, best["dec_sms"]), probe_read_bw(mux, part, wl, -1, total_sms)
     bw_part_mux = probe_read_bw_contended(mux, part, wl, i, best["dec_sms"], step_sides[0][0])
     tc_kp = time_tc_share(mux, part, wl, i, best["pf_sms"])
-    t_pf_k = time_kernel_alone(mux, part, wl, i, "pf")
+    t_pf_k, clk_pf_k = time_kernel_alone(mux, part, wl, i, "pf")
     qkv = None
     if wl.d == 128 and wl.Hq % 2 == 0 and wl.Hkv % 2 == 0:
         t_qkv, f_qkv = time_qkv_fused(mux, wl)
@@ -932,7 +937,7 @@ def main():
                "shape": f"T {wl.pf_spec.total_new}, hidden {wl.hidden}, inter 14336", "call_us": t_ffn * 1e6,
                "achieved": f_ffn / t_ffn / 1e12, "unit": "TFLOP/s", "peak": burst,
                "frac": f_ffn / t_ffn / 1e12 / burst, "note": "f4 second part, timed alone after the steps"}
-    t_dc_k = time_kernel_alone(mux, part, wl, i, "dc")
+    t_dc_k, clk_dc_k = time_kernel_alone(mux, part, wl, i, "dc")
     peak_pf = burst * pf_share
     roofline = {"bound": "tensor", "kernel": "prefill6_kernel (tcgen05 causal prefill attention, 1 launch per layer)",
                 "achieved": pf_tflops, "peak": peak_pf, "unit": "TFLOP/s", "frac": pf_tflops / peak_pf,
@@ -948,6 +953,7 @@ def main():
                              "green context, CUDA events, alone",
                 "vendor_peak_share": 2250.0 * pf_share, "frac_of_vendor_share": pf_tflops / (2250.0 * pf_share),
                 "alone_launch_us": t_pf_k * 1e6, "alone_frac": wl.prefill_flops_layer() / t_pf_k / 1e12 / peak_pf,
+                "alone_clocks": clk_pf_k,
                 "window": f"mean over the {len(pf_attn_ms)} prefill attention launches of the {K} timed steps "
                           "(decode side running beside it)"}
     roofline_dec = {"bound": "hbm", "kernel": "decode_kernel (+ combine_kernel when split)", "achieved": dc_gbs,
@@ -963,7 +969,7 @@ def main():
                     "sm_share": dc_share,
                     "iso_achieved": wl.decode_bytes_layer() / (best["t_dc_iso_ms"] * 1e-3 / NT) / 1e9,
                     "alone_launch_us": t_dc_k * 1e6, "alone_frac_of_partition_read": wl.decode_bytes_layer() / t_dc_k
-                    / 1e9 / bw_part}
+                    / 1e9 / bw_part, "alone_clocks": clk_dc_k}
     model = None
     if args.config in (2, 3, 5) and world == 1 and not args.no_model_step:
         try:

@@ -39,7 +39,7 @@ torch.cuda.synchronize()
 pf = np.concatenate([e.durations_ms(NT) for e in ev_pf]) * 1e3
 dc = np.concatenate([e.durations_ms(a.dc_layers) for e in ev_dc]) * 1e3
 tt = times.cpu().numpy()
-alone = bench.time_kernel_alone(mux, part, wl, 0, "pf") * 1e6
+alone = bench.time_kernel_alone(mux, part, wl, 0, "pf")[0] * 1e6
 print(f"step {e0.elapsed_time(e1) / K:.2f} ms | prefill attn {pf.mean():.1f} us (alone {alone:.1f}) | "
       f"decode attn {dc.mean():.1f} us | pf side {np.mean(tt[:, 3] - tt[:, 2]) * 1e-6:.2f} ms, "
       f"dc side {np.mean(tt[:, 1] - tt[:, 0]) * 1e-6:.2f} ms")
