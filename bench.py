@@ -907,15 +907,20 @@ def main():
     pf_tflops = wl.prefill_flops_layer() / pf_launch_s / 1e12
     dc_gbs = wl.decode_bytes_layer() / dc_launch_s / 1e9
     burst, sustained = peaks["bf16_tflops"], peaks.get("bf16_tflops_sustained", peaks["bf16_tflops"])
-    traffic = {}
-    for tf in ("r02q_traffic.json", "r02_traffic.json", "r01s3_traffic.json"):
+    traffic_files = []
+    for tf in ("r02z_traffic.json", "r02q_traffic.json", "r02_traffic.json", "r01s3_traffic.json"):
         try:
             with open(os.path.join(ROOT, "profiles", tf)) as f:
-                traffic = json.load(f)
-            traffic["_file"] = tf
-            break
+                traffic_files.append((tf, json.load(f)))
         except Exception:
             pass
+
+    def traffic_of(kernel):
+        """(DRAM bytes per launch, file) from the newest ncu --set full summary that has `kernel`."""
+        for tf, t in traffic_files:
+            if kernel in t:
+                return t[kernel].get("bytes"), tf
+        return None, None
     # SURVEY §8(d) decode denominators: BW_read(k_d) = read-only 32 KiB bulk-copy stream on the SAME
     # decode partition, alone and while the step's prefill side runs (contended: the primary one)
     bw_part, bw_full = probe_read_bw(mux, part, wl, i, best["dec_sms"]), probe_read_bw(mux, part, wl, -1, total_sms)
@@ -939,10 +944,15 @@ def main():
                "frac": f_ffn / t_ffn / 1e12 / burst, "note": "f4 second part, timed alone after the steps"}
     t_dc_k, clk_dc_k = time_kernel_alone(mux, part, wl, i, "dc")
     peak_pf = burst * pf_share
-    roofline = {"bound": "tensor", "kernel": "prefill6_kernel (tcgen05 causal prefill attention, 1 launch per layer)",
+    # which prefill kernel the library launches (prefill.cu launch_prefill): the persistent loop when the
+    # batch's K and V fit in 64 MiB of L2, else one CTA pair per work item
+    pf_persistent = sum(wl.pf_spec.L) * wl.Hkv * 4.0 * wl.d <= 64.0 * (1 << 20)
+    pf_kernel = "prefill6p_kernel" if pf_persistent else "prefill6_kernel"
+    roofline = {"bound": "tensor",
+                "kernel": pf_kernel + (" (tcgen05 causal prefill attention, persistent over the partition's SMs, "
+                                       if pf_persistent else " (tcgen05 causal prefill attention, ") + "1 launch per layer)",
                 "achieved": pf_tflops, "peak": peak_pf, "unit": "TFLOP/s", "frac": pf_tflops / peak_pf,
-                "traffic": (traffic.get("prefill6_kernel") or {}).get("bytes"),
-                "traffic_src": traffic.get("_file"),
+                "traffic": traffic_of(pf_kernel)[0], "traffic_src": traffic_of(pf_kernel)[1],
                 "launches": int(len(pf_attn_ms)), "launch_us_mean": pf_launch_s * 1e6,
                 "launch_us_p10_p90": [float(np.percentile(pf_attn_ms, q)) * 1e3 for q in (10, 90)],
                 "per_launch_flop": wl.prefill_flops_layer(),
@@ -959,7 +969,7 @@ def main():
     roofline_dec = {"bound": "hbm", "kernel": "decode_kernel (+ combine_kernel when split)", "achieved": dc_gbs,
                     "peak": bw_part_mux, "unit": "GB/s", "frac": dc_gbs / bw_part_mux,
                     "peak_src": f"BW_read({best['dec_sms']}) measured on the decode partition while the prefill side runs",
-                    "traffic": (traffic.get("decode_kernel") or {}).get("bytes"), "traffic_src": traffic.get("_file"),
+                    "traffic": traffic_of("decode_kernel")[0], "traffic_src": traffic_of("decode_kernel")[1],
                     "launches": int(len(dc_attn_ms)), "launch_us_mean": dc_launch_s * 1e6,
                     "per_launch_bytes": wl.decode_bytes_layer(),
                     "partition_read_alone_gbs": bw_part, "frac_of_partition_read_alone": dc_gbs / bw_part,

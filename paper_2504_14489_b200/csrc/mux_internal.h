@@ -225,6 +225,15 @@ __device__ __forceinline__ void tma_load_5d_mc(void* dst, const CUtensorMap* map
       "h"(mask)
       : "memory");
 }
+__device__ __forceinline__ void tma_load_5d_mc_hint(void* dst, const CUtensorMap* map, uint64_t* bar, int c0, int c1,
+                                                    int c2, int c3, int c4, uint16_t mask, uint64_t policy) {
+  asm volatile(
+      "cp.async.bulk.tensor.5d.shared::cluster.global.tile.mbarrier::complete_tx::bytes.multicast::cluster"
+      ".L2::cache_hint [%0], [%1, {%2, %3, %4, %5, %6}], [%7], %8, %9;" ::"r"(smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(c2), "r"(c3), "r"(c4), "r"(smem_u32(bar)),
+      "h"(mask), "l"(policy)
+      : "memory");
+}
 // ---- CTA pair (cluster of 2, tcgen05 cta_group::2) helpers
 __device__ __forceinline__ uint32_t cluster_ctarank() {
   uint32_t r;

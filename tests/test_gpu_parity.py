@@ -407,3 +407,43 @@ def test_decode_two_cta_small_partition_parity(mux, num_sms, Hq, Hkv, d):
         check_close(o_full.cpu().numpy(), ref, what=f"decode device launch, {ns} splits")
         if Hkv == 8:
             assert torch.equal(o, o_full), "small-partition launch != device launch"
+
+
+# persistent prefill loop (prefill6p_kernel): on a small green-context partition every
+# persistent unit walks many work items whose key-tile counts differ (1..nt_max), so the K / V ring
+# phases, the Q hand-over barrier and the O epilogue overlap run across items of every length
+@pytest.mark.parametrize("Hq,Hkv,r,n,dec_sms", [
+    (32, 8, [0, 1000, 17, 64, 300], [300, 1, 129, 700, 2], 132),   # g = 4: clusters of 2 on ~16 SMs
+    (12, 6, [5, 0, 260], [520, 131, 64], 128),                     # g = 2: single-CTA items on ~20 SMs
+    (8, 2, [0], [1000], 100),                                      # one sequence, 8 q tiles x 1 pair per unit
+])
+def test_prefill_persistent_on_partition(mux, Hq, Hkv, r, n, dec_sms):
+    import torch
+    d = 128
+    side = _side(90 + Hq + dec_sms, SideSpec(r, n), Hq, Hkv, d)
+    need = sum(side.spec.pages_needed())
+    gs = gpu_build_side(mux, side, need + 7, 13, Hkv, d)
+    os_ = oracle_build_side(side, need + 7, 13, Hkv, d)
+    scale = 1.0 / math.sqrt(d)
+    T = side.spec.total_new
+    part = mux.Partition(0, [dec_sms])
+    try:
+        _, psms, _, sp = part.query(0)
+        o = torch.empty((T, Hq, d), dtype=torch.float32, device="cuda")
+        lse = torch.empty((T, Hq), dtype=torch.float32, device="cuda")
+        o_full = torch.empty_like(o)
+        for _ in range(2):                 # a second launch over the same barriers' fresh phases
+            o.fill_(float("nan"))
+            mux.mux_prefill_attn(gs["pool"], 0, gs["batch"], Hq, gs["q"], o, lse, scale=scale, stream=sp)
+            torch.cuda.synchronize()
+        mux.mux_prefill_attn(gs["pool"], 0, gs["batch"], Hq, gs["q"], o_full, None, scale=scale)
+        torch.cuda.synchronize()
+    finally:
+        part.close()
+    assert psms <= 148 - dec_sms
+    # the same items on the whole device: bitwise the same (each item is computed by one CTA / pair)
+    assert torch.equal(o, o_full)
+    ref, ref_lse = oracle.attention(side.q, os_["kpool"], os_["vpool"], os_["qo_indptr"], os_["kv_len"],
+                                    os_["page_indptr"], os_["page_ids"], scale)
+    check_close(o.cpu().numpy(), ref, what=f"persistent prefill on {psms} SMs")
+    assert np.max(np.abs(lse.cpu().numpy() - ref_lse)) <= 1e-3
