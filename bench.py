@@ -853,8 +853,9 @@ def main():
              torch.empty(w.dc_y.shape, dtype=w.dc_y.dtype).pin_memory()] for w in sets]
     h2d = sum(t.numel() * t.element_size() for t in pin.values())
     d2h = sum(t.numel() * t.element_size() for t in outs[0])
-    cs = torch.cuda.Stream()
-    ev_in = [torch.cuda.Event(), torch.cuda.Event()]
+    cs = torch.cuda.Stream()                                 # H2D copy stream
+    cso = torch.cuda.Stream()                                # D2H copy stream: the two directions run on
+    ev_in = [torch.cuda.Event(), torch.cuda.Event()]        # separate copy engines (PCIe is full duplex)
     ev_done = [torch.cuda.Event(), torch.cuda.Event()]
     ev_out = [torch.cuda.Event(), torch.cuda.Event()]
 
@@ -876,15 +877,16 @@ def main():
             pfs, dcs = e2e_side(c, step)
             mux.mux_run_layer(part, i, wl.pool, pfs, dcs, wtimes)
             ev_done[c].record(st)
-            with torch.cuda.stream(cs):
-                cs.wait_event(ev_done[c])
+            with torch.cuda.stream(cso):
+                cso.wait_event(ev_done[c])
                 outs[c][0].copy_(sets[c].pf_y, non_blocking=True)
                 outs[c][1].copy_(sets[c].dc_y, non_blocking=True)
-                ev_out[c].record(cs)
+                ev_out[c].record(cso)
         st.wait_stream(cs)
+        st.wait_stream(cso)
 
     for e in ev_out:
-        e.record(cs)
+        e.record(cso)
     e2e_run(2)
     torch.cuda.synchronize()
     a2, b2 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
