@@ -725,13 +725,14 @@ def main():
             mux.mux_run_layer(part, i, wl.pool, pf, dc, times)
         torch.cuda.synchronize()
         st = torch.cuda.current_stream()
-        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        a.record(st)
-        for _ in range(reps):
+        evs = [torch.cuda.Event(enable_timing=True) for _ in range(reps + 1)]
+        evs[0].record(st)
+        for r_ in range(reps):
             mux.mux_run_layer(part, i, wl.pool, pf, dc, times)
-        b.record(st)
+            evs[r_ + 1].record(st)
         torch.cuda.synchronize()
-        t = a.elapsed_time(b) / reps * 1e-3
+        # median window: one power-cap clock dip in a rep must not decide the split
+        t = float(np.median([evs[r_].elapsed_time(evs[r_ + 1]) for r_ in range(reps)])) * 1e-3
         tt = times.cpu().numpy()
         entry.update({"t_mux_ms": t * 1e3, "tok_s": step_tokens(D) / t, "tbt_ms": t * 1e3 * NT / D,
                       "dec_side_ms": (tt[1] - tt[0]) * 1e-6, "pf_side_ms": (tt[3] - tt[2]) * 1e-6,
@@ -755,20 +756,41 @@ def main():
             continue
         seen.add(key)
         measure_mux(e)
-    # the paper's serving objective is goodput under SLOs: the split must keep a decode token's
-    # time between tokens (an iteration = N_T layers = N_T / D steps) within the TBT SLO
-    # (3 % margin: the timed steps run a little slower than the calibration's three)
-    ok = ([e for e in sweep if e["tbt_ms"] <= 0.97 * args.tbt_slo_ms] or
-          [e for e in sweep if e["tbt_ms"] <= args.tbt_slo_ms] or sweep)
-    # bubble-less: only splits whose two sides are busy for all but <= 5 % of the window
-    # on average (the idle share of the shorter side, halved); the fastest of those
-    for e in sweep:
-        e["bubble_pred"] = 0.5 * abs(e["dec_side_ms"] - e["pf_side_ms"]) / max(e["dec_side_ms"], e["pf_side_ms"])
-    ok = [e for e in ok if e["bubble_pred"] <= 0.05] or ok
-    best = max(ok, key=lambda e: e["tok_s"])
-    # among candidates within 1 % of the best rate, the most balanced sides
-    near = [e for e in ok if e["tok_s"] >= 0.99 * best["tok_s"]]
-    best = min(near, key=lambda e: abs(e["dec_side_ms"] - e["pf_side_ms"]) / max(e["dec_side_ms"], e["pf_side_ms"]))
+    def select(cands):
+        # the paper's serving objective is goodput under SLOs: the split must keep a decode token's
+        # time between tokens (an iteration = N_T layers = N_T / D steps) within the TBT SLO
+        # (3 % margin: the timed steps run a little slower than the calibration's three)
+        ok = ([e for e in cands if e["tbt_ms"] <= 0.97 * args.tbt_slo_ms] or
+              [e for e in cands if e["tbt_ms"] <= args.tbt_slo_ms] or cands)
+        # bubble-less: only splits whose two sides are busy for all but <= 5 % of the window
+        # on average (the idle share of the shorter side, halved); the fastest of those
+        for e in cands:
+            e["bubble_pred"] = 0.5 * abs(e["dec_side_ms"] - e["pf_side_ms"]) / max(e["dec_side_ms"], e["pf_side_ms"])
+        ok = [e for e in ok if e["bubble_pred"] <= 0.05] or ok
+        top = max(ok, key=lambda e: e["tok_s"])
+        # among candidates within 1 % of the best rate, the most balanced sides
+        near = [e for e in ok if e["tok_s"] >= 0.99 * top["tok_s"]]
+        return min(near, key=lambda e: abs(e["dec_side_ms"] - e["pf_side_ms"]) / max(e["dec_side_ms"], e["pf_side_ms"]))
+
+    best = select(sweep)
+    # refinement on the chosen split: every decode-layer count between the coarse candidates
+    # (0.7 r ... r), each re-measured over 7 windows (median); rank 0's list on every rank
+    r_best = best["t_pf_iso_ms"] / (best["t_dc_iso_ms"] / NT)
+    fine = list(range(max(1, int(round(0.7 * r_best))), int(round(r_best)) + 1))[:16]
+    if world > 1:
+        ft = torch.full((17,), -1, dtype=torch.int64, device="cuda")
+        ft[0] = sweep.index(best)
+        ft[1:1 + len(fine)] = torch.tensor(fine, dtype=torch.int64)
+        dist.broadcast(ft, 0)
+        best = sweep[int(ft[0].item())]
+        fine = [int(v) for v in ft[1:].tolist() if v >= 0]
+    refined = []
+    for Dn in fine:
+        e = {k_: best[k_] for k_ in ("split", "dec_sms", "pf_sms", "t_dc_iso_ms", "t_pf_iso_ms")}
+        e["dc_layers"] = Dn
+        refined.append(measure_mux(e, reps=7))
+    sweep = [e for e in sweep if e["split"] != best["split"]] + refined
+    best = select(sweep)
     if world > 1:  # every rank must run the same split: rank 0 decides
         t = torch.tensor([sweep.index(best)], device="cuda")
         dist.broadcast(t, 0)
