@@ -271,6 +271,7 @@ def test_engine_outputs_match_oracle_overlap(mux, part, overlap):
     eng.close()
 
 
+@pytest.mark.timing
 def test_engine_graphs_cut_launch_gap(mux, part):
     """f2: decode iterations as graph launches, enqueued one ahead (overlap),
     leave no host turn-around gap on the decode SMs between iterations; graph memory reported.
