@@ -932,7 +932,7 @@ def main():
     dc_gbs = wl.decode_bytes_layer() / dc_launch_s / 1e9
     burst, sustained = peaks["bf16_tflops"], peaks.get("bf16_tflops_sustained", peaks["bf16_tflops"])
     traffic_files = []
-    for tf in ("r02z_traffic.json", "r02q_traffic.json", "r02_traffic.json", "r01s3_traffic.json"):
+    for tf in ("r02o_traffic.json", "r02z_traffic.json", "r02q_traffic.json", "r02_traffic.json", "r01s3_traffic.json"):
         try:
             with open(os.path.join(ROOT, "profiles", tf)) as f:
                 traffic_files.append((tf, json.load(f)))
